@@ -1,0 +1,296 @@
+"""a2/a5/a7/a8/a9/a12/a13 -- state encoding, greedy / epsilon-greedy action selection, the
+vectorised environment step, replay, and the double-DQN update (ORACLE, test infra only).
+
+Paper: state = the W jobs of the window with their profile features; input layer
+W x (f + 5) (Table VI); ComputeRatio / MemoryRatio / DurationRatio = job value over the
+window mean; action = job set + partitioning; epsilon-greedy from 1 to 0.01,
+random actions from the whole search space, epsilon = 0 online; Q-learning update
+(P:178); duelling double DQN.  Experience replay and the vectorised env are
+required by BASELINE.json's north star (not in the paper).
+
+Readings: R10 the "+5" inputs = [c/cbar, m/mbar, T/Tbar, scheduled, U/W];
+R12 hyper-parameters; R13 deterministic transitions; R14 random action = k-th valid action;
+R15 fixed-point argmax with near-tie lockstep; R19 an episode = one window until every job is
+scheduled, then auto-reset from the host stream.
+
+Transition: s = (window, sched); a = (l, g, sigma) with g disjoint from sched;
+s' = (window, sched | bits(g)); done iff every job is scheduled (each job exactly once).
+
+Pins: tests/test_oracle_dqn.py -- epsilon = 1 -> every action is the k-th valid action,
+epsilon = 0 -> greedy; the explicit argmax equals a brute-force max over decode(idx);
+episodes schedule every job exactly once; replay index formula; the tabular special
+case of the Q-update rule; gamma = 0 / done -> y = r.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+from . import actions as A
+from . import corun as CR
+from . import qnet as QN
+
+NEAR_TIE = 1e-4  # reading R15: argmax mismatch allowed iff oracle gap <= 1e-4 max(1, |Q|)
+
+
+class Tables:
+    """Per-space enumeration tables in index order (plain products of itertools orders)."""
+
+    def __init__(self, space):
+        self.space = space
+        self.off = A.offsets(space)
+        W = space.W
+        self.members = {}
+        self.slot_of = {}
+        self.gmask = {}
+        for C in sorted({l.C for l in space.layouts}):
+            mem, so, gm = [], [], []
+            for g in itertools.combinations(range(W), C):
+                m = A.group_mask(g)
+                for sg in itertools.permutations(range(C)):
+                    mem.append(g)
+                    so.append(sg)
+                    gm.append(m)
+            self.members[C] = np.array(mem, np.int64).reshape(-1, C)
+            self.slot_of[C] = np.array(so, np.int64).reshape(-1, C)
+            self.gmask[C] = np.array(gm, np.uint64)
+
+
+def encode(window, sched: int, pool, W: int) -> np.ndarray:
+    """x = W rows of [features (f) | c/cbar, m/mbar, T/Tbar | scheduled | U/W]."""
+    ids = [int(x) for x in window]
+    c = np.array([float(pool.compute_pm[j]) for j in ids])
+    m = np.array([float(pool.memory_pm[j]) for j in ids])
+    T = np.array([float(pool.solo_ticks[j]) for j in ids])
+    sbit = np.array([float((sched >> j) & 1) for j in range(W)])
+    U = W - int(sbit.sum())
+    rows = []
+    for j in range(W):
+        rows.append(np.concatenate([pool.features[ids[j]].astype(np.float64),
+                                    [c[j] / c.mean(), m[j] / m.mean(), T[j] / T.mean(),
+                                     sbit[j], U / W]]))
+    return np.concatenate(rows)
+
+
+def head_fixed(z, space):
+    v, aL, aJ = QN.split_head(np.asarray(z, np.float64), space)
+    cL, cJ = QN.center(aL, aJ)
+    Fv = QN.fixed(v)
+    FcL = [QN.fixed(x) for x in cL]
+    FcJ = [[QN.fixed(x) for x in row] for row in cJ]
+    return v, cL, cJ, Fv, FcL, FcJ
+
+
+def greedy_explicit(tab: Tables, Fv, FcL, FcJ, sched: int):
+    """argmax over every valid action of Q^ (exact integers), ties to the lowest index.
+    Returns (idx, Q^max) or (-1, None) when no action is valid."""
+    sp = tab.space
+    FJ = np.array(FcJ, dtype=np.int64)
+    assert np.abs(FJ).max(initial=0) < (1 << 58)
+    best, best_idx = None, -1
+    for l, lay in enumerate(sp.layouts):
+        C = lay.C
+        mem, so, gm = tab.members[C], tab.slot_of[C], tab.gmask[C]
+        valid = (gm & np.uint64(sched)) == 0
+        if not valid.any():
+            continue
+        types = np.array(sp.slot_type[l], np.int64)[so]          # [n][C]
+        score = np.full(len(mem), FcL[l] + Fv, dtype=np.int64)
+        for i in range(C):
+            score += FJ[mem[:, i], types[:, i]]
+        score = np.where(valid, score, np.iinfo(np.int64).min)
+        k = int(np.argmax(score))                                 # first max = lowest idx
+        s = int(score[k])
+        if best is None or s > best:
+            best, best_idx = s, tab.off[l] + k
+    return best_idx, best
+
+
+class OracleDQN:
+    """The vectorised DQN environment + agent of SURVEY §8(c) Q1-Q4, one rank."""
+
+    def __init__(self, space, pool, net, theta0, n_envs, batch, replay_capacity,
+                 gamma=0.99, lr=1e-3, reward_lambda=0.0, q3=1, greedy=None):
+        self.sp = space
+        self.pool = pool
+        self.tab = Tables(space) if greedy is None else None
+        self.greedy_fn = greedy or (lambda Fv, FcL, FcJ, sched:
+                                    greedy_explicit(self.tab, Fv, FcL, FcJ, sched))
+        self.off = A.offsets(space)
+        self.dims = QN.net_dims(space, net)
+        self.theta = np.asarray(theta0, np.float64).copy()
+        self.theta_t = self.theta.copy()
+        self.E, self.B, self.N = n_envs, batch, replay_capacity
+        self.gamma, self.lr, self.lam, self.q3 = gamma, lr, reward_lambda, q3
+        self.windows = None
+        self.sched = None
+        self.rep_win = np.zeros((self.N, space.W), np.uint8)
+        self.rep_sched = np.zeros(self.N, np.uint64)
+        self.rep_act = np.zeros(self.N, np.int64)
+        self.rep_r = np.zeros(self.N, np.float64)
+        self.rep_done = np.zeros(self.N, np.uint8)
+        self.inserted = 0
+        self.t = 0
+        self.near_ties = 0
+
+    # -- helpers -----------------------------------------------------------------------
+    def _heads(self, theta, windows, scheds):
+        X = np.stack([encode(w, int(s), self.pool, self.sp.W) for w, s in zip(windows, scheds)])
+        z, acts = QN.forward(theta, self.dims, X)
+        return z, acts
+
+    def _adopt(self, mine, theirs, Fv, FcL, FcJ, qmax, sched):
+        """Near-tie lockstep (reading R15): adopt the GPU's action if our Q^ gap <= 1e-4."""
+        if theirs is None or theirs == mine:
+            return mine, 0
+        theirs = int(theirs)
+        l, g, sg = A.decode(self.sp, theirs, self.off)
+        if A.group_mask(g) & sched:
+            raise AssertionError(f"GPU chose invalid action {theirs}")
+        qt = QN.q_fixed(Fv, FcL, FcJ, self.sp, l, g, sg)
+        gap = (qmax - qt) / 4294967296.0
+        if gap <= NEAR_TIE * max(1.0, abs(qmax / 4294967296.0)):
+            self.near_ties += 1
+            return theirs, 1
+        raise AssertionError(f"argmax mismatch: oracle {mine} gpu {theirs} gap {gap}")
+
+    # -- API mirrored by libhrp ---------------------------------------------------------
+    def reset(self, windows):
+        self.windows = np.array(windows, np.uint8).copy()
+        self.sched = np.zeros(len(windows), np.uint64)
+
+    def q_forward(self, windows, scheds, gpu_argmax=None):
+        z, _ = self._heads(self.theta, windows, scheds)
+        out_a, out_q = [], []
+        for b in range(len(windows)):
+            v, cL, cJ, Fv, FcL, FcJ = head_fixed(z[b], self.sp)
+            a, q = self.greedy_fn(Fv, FcL, FcJ, int(scheds[b]))
+            if gpu_argmax is not None and a >= 0:
+                a, _ = self._adopt(a, gpu_argmax[b], Fv, FcL, FcJ, q, int(scheds[b]))
+                q = q_fixed_idx_any(self.sp, self.off, Fv, FcL, FcJ, a)
+            out_a.append(a)
+            out_q.append(q / 4294967296.0 if q is not None else float("nan"))
+        return np.array(out_a, np.int64), np.array(out_q), z
+
+    def env_step(self, thr, u_explore, u_action, next_windows, gpu_actions=None):
+        E, sp = self.E, self.sp
+        z, _ = self._heads(self.theta, self.windows, self.sched)
+        acts = np.zeros(E, np.int64)
+        rew = np.zeros(E)
+        done = np.zeros(E, np.uint8)
+        cor = np.zeros(E, np.int64)
+        qsel = np.zeros(E)
+        for e in range(E):
+            sched = int(self.sched[e])
+            v, cL, cJ, Fv, FcL, FcJ = head_fixed(z[e], sp)
+            if int(u_explore[e]) < int(thr):
+                nv = A.n_valid(sp, sched)
+                a = A.kth_valid(sp, sched, A.explore_k(int(u_action[e]), nv), self.off)
+            else:
+                a, q = self.greedy_fn(Fv, FcL, FcJ, sched)
+                if gpu_actions is not None:
+                    a, _ = self._adopt(a, gpu_actions[e], Fv, FcL, FcJ, q, sched)
+            l, g, sg = A.decode(sp, a, self.off)
+            assert A.group_mask(g) & sched == 0
+            r, cr, solo = CR.reward(sp.layouts[l], g, sg, self.windows[e], self.pool,
+                                    self.lam, self.q3)
+            qsel[e] = QN.q_fixed(Fv, FcL, FcJ, sp, l, g, sg) / 4294967296.0
+            s2 = sched | A.group_mask(g)
+            d = int(s2 == (1 << sp.W) - 1)
+            slot = (self.t * E + e) % self.N
+            self.rep_win[slot] = self.windows[e]
+            self.rep_sched[slot] = np.uint64(sched)
+            self.rep_act[slot] = a
+            self.rep_r[slot] = r
+            self.rep_done[slot] = d
+            acts[e], rew[e], done[e], cor[e] = a, r, d, cr
+            if d:
+                self.windows[e] = next_windows[e]
+                self.sched[e] = np.uint64(0)
+            else:
+                self.sched[e] = np.uint64(s2)
+        self.inserted += E
+        self.t += 1
+        return acts, rew, done, cor, qsel
+
+    def sample(self, u_replay):
+        nf = min(self.N, self.inserted)
+        return np.array([(int(u) * nf) >> 32 for u in u_replay], np.int64)
+
+    def dqn_update(self, u_replay, sync_target, gpu_astar=None, b_total=None, apply=True):
+        """One double-DQN step on a replay batch.  Returns a dict with loss, idx, a*, y,
+        Q(s,a), grad (sum-form / B_total).  With apply=False the caller applies the SGD
+        step (multi-rank simulation)."""
+        sp, B = self.sp, len(u_replay)
+        b_total = b_total or B
+        idx = self.sample(u_replay)
+        win = self.rep_win[idx]
+        sch = self.rep_sched[idx].astype(np.uint64)
+        act = self.rep_act[idx]
+        r = self.rep_r[idx]
+        dn = self.rep_done[idx]
+        dec = [A.decode(sp, int(a), self.off) for a in act]
+        sch2 = np.array([int(s) | A.group_mask(g) for s, (_, g, _) in zip(sch, dec)],
+                        np.uint64)
+        z_s, acts = self._heads(self.theta, win, sch)
+        z_n, _ = self._heads(self.theta, win, sch2)
+        z_t, _ = self._heads(self.theta_t, win, sch2)
+        astar = np.full(B, -1, np.int64)
+        y = np.zeros(B)
+        q_sa = np.zeros(B)
+        dz = np.zeros_like(z_s)
+        for b in range(B):
+            if not dn[b]:
+                v, cL, cJ, Fv, FcL, FcJ = head_fixed(z_n[b], sp)
+                a2, q2 = self.greedy_fn(Fv, FcL, FcJ, int(sch2[b]))
+                if gpu_astar is not None:
+                    a2, _ = self._adopt(a2, gpu_astar[b], Fv, FcL, FcJ, q2, int(sch2[b]))
+                astar[b] = a2
+                vt, aLt, aJt = QN.split_head(z_t[b], sp)
+                cLt, cJt = QN.center(aLt, aJt)
+                l2, g2, s2 = A.decode(sp, int(a2), self.off)
+                qt = QN.q_value(vt, cLt, cJt, sp, l2, g2, s2)
+                y[b] = r[b] + self.gamma * qt
+            else:
+                y[b] = r[b]
+            v, aL, aJ = QN.split_head(z_s[b], sp)
+            cL, cJ = QN.center(aL, aJ)
+            l, g, sg = dec[b]
+            q_sa[b] = QN.q_value(v, cL, cJ, sp, l, g, sg)
+            dz[b] = QN.dq_dz(sp, l, g, sg) * (q_sa[b] - y[b]) / b_total
+        delta = q_sa - y
+        loss = float((delta ** 2).sum() / (2 * B))
+        grad = QN.backward(self.theta, self.dims, acts, dz)
+        if apply:
+            self.apply(grad, sync_target)
+        return {"loss": loss, "idx": idx, "astar": astar, "y": y, "q_sa": q_sa,
+                "grad": grad}
+
+    def apply(self, grad, sync_target):
+        self.theta = self.theta - self.lr * grad
+        if sync_target:
+            self.theta_t = self.theta.copy()
+
+
+def q_fixed_idx_any(space, off, Fv, FcL, FcJ, idx):
+    l, g, sg = A.decode(space, int(idx), off)
+    return QN.q_fixed(Fv, FcL, FcJ, space, l, g, sg)
+
+
+def greedy_bruteforce(space, Fv, FcL, FcJ, sched):
+    """Literal definition for tiny spaces: decode every index, keep the first maximum."""
+    off = A.offsets(space)
+    best, bi = None, -1
+    for idx in range(off[-1]):
+        l, g, sg = A.decode(space, idx, off)
+        if A.group_mask(g) & sched:
+            continue
+        q = QN.q_fixed(Fv, FcL, FcJ, space, l, g, sg)
+        if best is None or q > best:
+            best, bi = q, idx
+    return bi, best
+
+
+__all__ = ["Tables", "encode", "head_fixed", "greedy_explicit", "greedy_bruteforce",
+           "OracleDQN", "NEAR_TIE"]

@@ -1,0 +1,161 @@
+"""Pins for oracle/env.py (encode, argmax, epsilon-greedy step, replay, DQN update)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import actions as A
+from oracle import env as EV
+from oracle import qnet as QN
+from oracle import space as SP
+from synth.configs import NetCfg
+
+
+def _rand_heads(sp, rng, ties=True):
+    Fv = int(rng.integers(-5, 5))
+    hi = 4 if ties else 1 << 20
+    FcL = [int(x) for x in rng.integers(-hi, hi, sp.L)]
+    FcJ = [[int(x) for x in row] for row in rng.integers(-hi, hi, (sp.W, sp.T))]
+    return Fv, FcL, FcJ
+
+
+@pytest.mark.parametrize("W,cmax,S", [(4, 2, (25, 50, 75)), (5, 3, (25, 50, 75)),
+                                      (4, 4, (50,))])
+def test_explicit_argmax_equals_literal(W, cmax, S):
+    # literal definition: decode every index, keep the first maximum over valid ones
+    sp = SP.build_space(W, cmax, S)
+    tab = EV.Tables(sp)
+    rng = np.random.default_rng(3)
+    for _ in range(40):
+        Fv, FcL, FcJ = _rand_heads(sp, rng)
+        sched = int(rng.integers(0, (1 << W) - 1))
+        assert EV.greedy_explicit(tab, Fv, FcL, FcJ, sched) == \
+            EV.greedy_bruteforce(sp, Fv, FcL, FcJ, sched)
+
+
+def test_encode_layout_and_ratios():
+    pool = synth.make_pool(27)
+    win = [0, 9, 20, 3]
+    x = EV.encode(win, 0b0101, pool, 4).reshape(4, 17)
+    np.testing.assert_array_equal(x[:, :12], pool.features[win].astype(np.float64))
+    c = pool.compute_pm[win].astype(float)
+    np.testing.assert_allclose(x[:, 12], c / c.mean())
+    assert x[:, 12].mean() == pytest.approx(1.0)   # ratio to the window mean
+    assert x[:, 13].mean() == pytest.approx(1.0)
+    assert x[:, 14].mean() == pytest.approx(1.0)
+    assert list(x[:, 15]) == [1, 0, 1, 0]
+    assert list(x[:, 16]) == [0.5] * 4
+
+
+def _agent(cfgk=1, E=16, B=8, net=None, lam=0.0, gamma=0.99, lr=1e-3, W=None):
+    cfg = synth.config(cfgk)
+    sc = cfg.space
+    sp = SP.build_space(W or sc.window, sc.cmax, sc.shares)
+    pool = synth.make_pool(cfg.pool)
+    net = net or cfg.net
+    dims = QN.net_dims(sp, net)
+    theta = synth.init_weights(dims)
+    ag = EV.OracleDQN(sp, pool, net, theta, E, B, 1 << 10, gamma=gamma, lr=lr,
+                      reward_lambda=lam)
+    ag.reset(synth.make_windows(pool, E, sp.W))
+    return ag, sp, pool
+
+
+def test_episodes_schedule_every_job_exactly_once():
+    # the job sets partition Q (each job exactly once), 1 <= C_i <= Cmax
+    ag, sp, pool = _agent(E=24)
+    W = sp.W
+    used = [0] * ag.E
+    finished = 0
+    for t in range(12):
+        st = synth.step_streams(t, ag.E, ag.B, W, pool)
+        thr = synth.eps_threshold(t, 6)
+        win_before = ag.windows.copy()
+        a, r, d, cr, q = ag.env_step(thr, st["u_explore"], st["u_action"],
+                                     st["next_windows"])
+        for e in range(ag.E):
+            l, g, s = A.decode(sp, int(a[e]))
+            m = A.group_mask(g)
+            assert used[e] & m == 0
+            assert 1 <= len(g) <= sp.cmax
+            used[e] |= m
+            if d[e]:
+                assert used[e] == (1 << W) - 1
+                used[e] = 0
+                finished += 1
+                np.testing.assert_array_equal(ag.windows[e], st["next_windows"][e])
+            else:
+                np.testing.assert_array_equal(ag.windows[e], win_before[e])
+    assert finished > 0
+
+
+def test_epsilon_one_is_kth_valid_and_zero_is_greedy():
+    ag, sp, pool = _agent(E=16)
+    st = synth.step_streams(0, ag.E, ag.B, sp.W, pool)
+    a1, *_ = ag.env_step(1 << 32, st["u_explore"], st["u_action"], st["next_windows"])
+    for e in range(ag.E):
+        nv = A.n_valid(sp, 0)
+        assert a1[e] == A.kth_valid(sp, 0, A.explore_k(int(st["u_action"][e]), nv))
+    # eps = 0: every action is the argmax of the online net
+    ag2, sp, pool = _agent(E=16)
+    z, _ = ag2._heads(ag2.theta, ag2.windows, ag2.sched)
+    a0, *_ = ag2.env_step(0, st["u_explore"], st["u_action"], st["next_windows"])
+    for e in range(ag2.E):
+        _, _, _, Fv, FcL, FcJ = EV.head_fixed(z[e], sp)
+        assert a0[e] == EV.greedy_bruteforce(sp, Fv, FcL, FcJ, 0)[0]
+
+
+def test_replay_sample_index_uniform():
+    ag, sp, pool = _agent(E=16)
+    ag.inserted = 1000
+    rng = np.random.default_rng(5)
+    u = rng.integers(0, 1 << 32, 200000, dtype=np.uint64)
+    idx = ag.sample(u)
+    assert idx.min() >= 0 and idx.max() < 1000
+    counts = np.bincount(idx, minlength=1000)
+    chi2 = ((counts - 200.0) ** 2 / 200.0).sum()
+    assert chi2 < 1000 + 6 * np.sqrt(2000)
+
+
+def test_tabular_update_rule_special_case():
+    # Q_new(s,a) = Q(s,a) + alpha (r + gamma max Q(s',.) - Q(s,a)).  With W = 1 (the
+    # job-advantage terms cancel), no hidden layer, batch 1 and plain SGD on (1/2) delta^2,
+    # the change of Q(s,a) is exactly alpha (y - Q) with alpha = lr (2 - 1/L) (|x|^2 + 1).
+    cfg = synth.config(1)
+    sp = SP.build_space(1, 1, (25, 50, 75))
+    pool = synth.make_pool(27)
+    net = NetCfg(0, 0)
+    dims = QN.net_dims(sp, net)
+    assert dims == [17, sp.H]
+    rng = np.random.default_rng(7)
+    theta = rng.normal(0, 0.1, QN.n_params(dims))
+    for gamma in (0.0, 0.9):
+        ag = EV.OracleDQN(sp, pool, net, theta, 1, 1, 64, gamma=gamma, lr=0.01)
+        ag.reset([[5]])
+        ag.env_step(1 << 32, [0], [123456789 << 20], [[7]])      # explore, done
+        assert ag.rep_done[0] == 1
+        x = EV.encode([5], 0, pool, 1)
+        z0, _ = QN.forward(ag.theta, dims, x[None])
+        l, g, s = A.decode(sp, int(ag.rep_act[0]))
+        v, aL, aJ = QN.split_head(z0[0], sp)
+        cL, cJ = QN.center(aL, aJ)
+        q0 = QN.q_value(v, cL, cJ, sp, l, g, s)
+        out = ag.dqn_update([0], False)
+        y = ag.rep_r[0]                                # done -> y = r (no bootstrap)
+        assert out["y"][0] == pytest.approx(y, abs=1e-12)
+        z1, _ = QN.forward(ag.theta, dims, x[None])
+        v, aL, aJ = QN.split_head(z1[0], sp)
+        cL, cJ = QN.center(aL, aJ)
+        q1 = QN.q_value(v, cL, cJ, sp, l, g, s)
+        alpha = 0.01 * (2 - 1 / sp.L) * (x @ x + 1)
+        assert q1 == pytest.approx(q0 + alpha * (y - q0), rel=1e-10, abs=1e-10)
+
+
+def test_gamma_zero_target_is_reward():
+    ag, sp, pool = _agent(E=8, B=8, gamma=0.0)
+    for t in range(3):
+        st = synth.step_streams(t, ag.E, ag.B, sp.W, pool)
+        ag.env_step(synth.eps_threshold(t, 5), st["u_explore"], st["u_action"],
+                    st["next_windows"])
+    st = synth.step_streams(9, ag.E, ag.B, sp.W, pool)
+    out = ag.dqn_update(st["u_replay"], False)
+    np.testing.assert_allclose(out["y"], ag.rep_r[out["idx"]], atol=0)
