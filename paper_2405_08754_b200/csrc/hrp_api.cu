@@ -1,0 +1,784 @@
+// libhrp: C ABI entry points (include/hrp.h), context management and kernel launches.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hrp.h"
+#include "tables.h"
+#include "dev.cuh"
+
+#include "k_gemm_simt.cuh"
+#include "k_env.cuh"
+#include "k_brute.cuh"
+#include "gemm_tc.h"
+
+using namespace hrp;
+
+namespace {
+
+thread_local std::string g_err;
+
+hrp_status fail(hrp_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(HRP_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+#define CKN(call)                                                                    \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess)                                                           \
+      return fail(HRP_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_));    \
+  } while (0)
+
+bool g_const_ready[64] = {false};
+
+hrp_status init_constants(int device) {
+  if (device >= 0 && device < 64 && g_const_ready[device]) return HRP_OK;
+  int64_t b[65][5];
+  for (int n = 0; n <= 64; ++n)
+    for (int k = 0; k <= 4; ++k) b[n][k] = binom(n, k);
+  int64_t f[5] = {1, 1, 2, 6, 24};
+  CK(cudaMemcpyToSymbol(c_binom, b, sizeof(b)));
+  CK(cudaMemcpyToSymbol(c_fact, f, sizeof(f)));
+  if (device >= 0 && device < 64) g_const_ready[device] = true;
+  return HRP_OK;
+}
+
+// RAII-free device arena: all allocations freed in ctx destruction.
+struct Arena {
+  std::vector<void*> ptrs;
+  cudaError_t alloc(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+  void release() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+template <class T>
+cudaError_t upload(Arena& ar, T** dst, const T* src, size_t n, cudaStream_t st) {
+  cudaError_t e = ar.alloc((void**)dst, n * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (n) e = cudaMemcpyAsync(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice, st);
+  return e;
+}
+
+hrp_status validate_pool(const hrp_profiles* p) {
+  if (!p) return fail(HRP_EINVAL, "profiles is NULL");
+  if (p->n_jobs < 1 || p->n_jobs > kMaxP) return fail(HRP_ERANGE, "n_jobs must be in 1..256");
+  if (p->n_features != kF) return fail(HRP_EINVAL, "n_features must be 12 (Table III)");
+  if (!p->solo_ticks || !p->compute_pm || !p->memory_pm || !p->features)
+    return fail(HRP_EINVAL, "profile array is NULL");
+  for (int i = 0; i < p->n_jobs; ++i) {
+    if (p->solo_ticks[i] < 1 || p->solo_ticks[i] >= (int64_t(1) << 31))
+      return fail(HRP_ERANGE, "solo_ticks must be in 1..2^31-1");
+    if (p->compute_pm[i] < 1 || p->compute_pm[i] > 1000 || p->memory_pm[i] < 1 ||
+        p->memory_pm[i] > 1000)
+      return fail(HRP_ERANGE, "compute_pm / memory_pm must be in 1..1000");
+  }
+  return HRP_OK;
+}
+
+// Device copies of space + pool tables.
+struct DevTables {
+  DevSpace sp{};
+  DevPool pool{};
+};
+
+hrp_status upload_tables(const HostSpace& hs, const hrp_profiles* prof, bool combos, Arena& ar,
+                         cudaStream_t st, DevTables& out,
+                         std::vector<std::vector<uint8_t>>* keep = nullptr) {
+  const int L = hs.L, T = hs.T, W = hs.W;
+  std::vector<uint8_t> n(L), ndom(L);
+  std::vector<uint32_t> stype(L), slot(L * 4, 0);
+  for (int l = 0; l < L; ++l) {
+    n[l] = (uint8_t)hs.nslots[l];
+    uint32_t t = 0;
+    uint32_t dm = 0;
+    for (int k = 0; k < hs.nslots[l]; ++k) {
+      t |= (uint32_t)hs.stype[l][k] << (8 * k);
+      const hrp_slot& s = hs.slots[l][k];
+      slot[l * 4 + k] = (uint32_t)s.sm800 | (uint32_t)s.b8 << 16 | (uint32_t)s.domain << 24;
+      dm |= 1u << s.domain;
+    }
+    stype[l] = t;
+    ndom[l] = (uint8_t)__builtin_popcount(dm);
+  }
+  std::vector<uint16_t> tsm(T);
+  std::vector<uint8_t> tb8(T);
+  for (int t = 0; t < T; ++t) {
+    tsm[t] = (uint16_t)hs.types[t].first;
+    tb8[t] = (uint8_t)hs.types[t].second;
+  }
+  DevSpace& d = out.sp;
+  d.W = W; d.cmax = hs.cmax; d.L = L; d.T = T; d.H = hs.head_width(); d.q3 = hs.q3;
+  d.n_actions = hs.n_actions();
+  CK(upload(ar, (uint8_t**)&d.lay_n, n.data(), L, st));
+  CK(upload(ar, (uint8_t**)&d.lay_ndom, ndom.data(), L, st));
+  CK(upload(ar, (uint32_t**)&d.lay_stype, stype.data(), L, st));
+  CK(upload(ar, (uint32_t**)&d.lay_slot, slot.data(), slot.size(), st));
+  CK(upload(ar, (int64_t**)&d.off, hs.off.data(), hs.off.size(), st));
+  CK(upload(ar, (uint16_t**)&d.type_sm800, tsm.data(), T, st));
+  CK(upload(ar, (uint8_t**)&d.type_b8, tb8.data(), T, st));
+  for (int C = 0; C < 5; ++C) {
+    d.combo[C] = nullptr;
+    d.combo_mask[C] = nullptr;
+    d.ncombo[C] = 0;
+    d.nlay_c[C] = 0;
+  }
+  for (int l = 0; l < L; ++l) d.nlay_c[hs.nslots[l]]++;
+  if (combos) {
+    for (int C = 1; C <= hs.cmax; ++C) {
+      std::vector<uint32_t> mem;
+      std::vector<uint64_t> msk;
+      std::vector<int> g(C);
+      for (int i = 0; i < C; ++i) g[i] = i;
+      while (true) {
+        uint32_t pk = 0;
+        uint64_t m = 0;
+        for (int i = 0; i < C; ++i) {
+          pk |= (uint32_t)g[i] << (8 * i);
+          m |= 1ull << g[i];
+        }
+        mem.push_back(pk);
+        msk.push_back(m);
+        int i = C - 1;
+        while (i >= 0 && g[i] == W - C + i) --i;
+        if (i < 0) break;
+        ++g[i];
+        for (int j = i + 1; j < C; ++j) g[j] = g[j - 1] + 1;
+      }
+      d.ncombo[C] = (int)mem.size();
+      CK(upload(ar, (uint32_t**)&d.combo[C], mem.data(), mem.size(), st));
+      CK(upload(ar, (uint64_t**)&d.combo_mask[C], msk.data(), msk.size(), st));
+    }
+  }
+  // pool + co-run compute-term table tc[p][tau] = ceil(T max(5 sm800, 4c) / (5 sm800)) (R8)
+  const int P = prof->n_jobs;
+  std::vector<int64_t> tc((size_t)P * T);
+  for (int p = 0; p < P; ++p)
+    for (int t = 0; t < T; ++t) {
+      const int64_t s5 = 5 * (int64_t)hs.types[t].first;
+      const int64_t c4 = 4 * (int64_t)prof->compute_pm[p];
+      const int64_t num = prof->solo_ticks[p] * std::max(s5, c4);
+      tc[(size_t)p * T + t] = (num + s5 - 1) / s5;
+    }
+  DevPool& q = out.pool;
+  q.P = P;
+  CK(upload(ar, (float**)&q.feat, prof->features, (size_t)P * kF, st));
+  CK(upload(ar, (int64_t**)&q.T, prof->solo_ticks, P, st));
+  CK(upload(ar, (int16_t**)&q.c, prof->compute_pm, P, st));
+  CK(upload(ar, (int16_t**)&q.m, prof->memory_pm, P, st));
+  CK(upload(ar, (int64_t**)&q.tc, tc.data(), tc.size(), st));
+  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+  (void)keep;
+  return HRP_OK;
+}
+
+}  // namespace
+
+struct hrp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  hrp_train_cfg cfg{};
+  HostSpace hs;
+  DevTables dt;
+  Arena ar;
+  bool explicit_mode = true;
+  int gemm_mode = 1;
+  // network
+  std::vector<int> dims;     // layer widths: in, w.., H
+  std::vector<int64_t> woff; // per layer offset of W in the flat params
+  int64_t n_params = 0;
+  float *theta = nullptr, *theta_t = nullptr, *grad = nullptr, *ws_splitk = nullptr;
+  size_t ws_splitk_elems = 0;
+  // env state
+  uint8_t* win = nullptr;
+  uint64_t* sched = nullptr;
+  // replay
+  uint8_t* rep_win = nullptr;
+  uint64_t* rep_sched = nullptr;
+  int64_t* rep_act = nullptr;
+  float* rep_r = nullptr;
+  uint8_t* rep_done = nullptr;
+  int64_t t = 0, inserted = 0;
+  // workspaces
+  int rows_max = 0;
+  float* X = nullptr;                 // [rows][in]
+  std::vector<float*> act;            // hidden outputs [rows][w] per layer
+  float* z = nullptr;                 // [rows][H]
+  float* zt = nullptr;                // [B][H]
+  float* dz = nullptr;                // [B][H]
+  float *dh0 = nullptr, *dh1 = nullptr;  // [B][w]
+  uint8_t* bwin = nullptr;            // [2B][W] or [chunk][W]
+  uint64_t* bsched = nullptr;
+  int64_t* bact = nullptr;
+  float* br = nullptr;
+  uint8_t* bdone = nullptr;
+  float* dsq = nullptr;
+  int64_t* tmp_i64 = nullptr;         // [rows]
+  unsigned long long* n_evals = nullptr;
+  size_t sel_smem = 0;
+  int sel_grid = 0;
+  int64_t launches = 0;
+  TcGemm* tc = nullptr;
+};
+
+namespace {
+
+hrp_status launch_check(hrp_ctx* c) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HRP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return HRP_OK;
+}
+
+// C = epi(A . B) with the SIMT kernel; split-K (EPI_STORE) when `splitk_out` is set.
+template <bool AK, bool BKc, int EPI>
+hrp_status sgemm(hrp_ctx* c, int M, int N, int K, const float* A, int lda, const float* B,
+                 int ldb, float* C, int ldc, const float* bias, const float* aux, int ldaux) {
+  const int64_t t128 = (int64_t)((M + 127) / 128) * ((N + 127) / 128);
+  if (EPI != EPI_STORE && t128 >= 2 * 148) {
+    dim3 grid((N + 127) / 128, (M + 127) / 128, 1);
+    sgemm_kernel<128, 128, 8, 8, AK, BKc, EPI><<<grid, 256, 0, c->stream>>>(
+        M, N, K, A, lda, B, ldb, C, ldc, bias, aux, ldaux, K);
+    return launch_check(c);
+  }
+  const int64_t t64 = (int64_t)((M + 63) / 64) * ((N + 63) / 64);
+  if (EPI != EPI_STORE) {
+    dim3 grid((N + 63) / 64, (M + 63) / 64, 1);
+    sgemm_kernel<64, 64, 4, 4, AK, BKc, EPI><<<grid, 256, 0, c->stream>>>(
+        M, N, K, A, lda, B, ldb, C, ldc, bias, aux, ldaux, K);
+    return launch_check(c);
+  }
+  // split-K into the workspace, then a deterministic reduce into C (ldc == N)
+  int S = (int)std::min<int64_t>(32, std::max<int64_t>(1, (2 * 148 + t64 - 1) / t64));
+  int kc = (K + S - 1) / S;
+  kc = (kc + 7) / 8 * 8;
+  S = (K + kc - 1) / kc;
+  if ((size_t)S * M * N > c->ws_splitk_elems) return fail(HRP_ENOMEM, "split-K workspace too small");
+  dim3 grid((N + 63) / 64, (M + 63) / 64, S);
+  sgemm_kernel<64, 64, 4, 4, AK, BKc, EPI_STORE><<<grid, 256, 0, c->stream>>>(
+      M, N, K, A, lda, B, ldb, c->ws_splitk, N, bias, aux, ldaux, kc);
+  hrp_status s = launch_check(c);
+  if (s) return s;
+  const int64_t n = (int64_t)M * N;
+  splitk_reduce_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(
+      S, n, c->ws_splitk, C);
+  return launch_check(c);
+}
+
+// Forward of one network over M rows of X.  If keep, hidden outputs go to c->act (for the
+// backward pass); z_out [M][H].
+hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out) {
+  const int nl = (int)c->dims.size() - 1;
+  const float* h = X;
+  for (int i = 0; i < nl; ++i) {
+    const int fi = c->dims[i], fo = c->dims[i + 1];
+    const float* Wm = theta + c->woff[i];
+    const float* b = Wm + (int64_t)fi * fo;
+    float* out = (i == nl - 1) ? z_out : c->act[i];
+    hrp_status s;
+    if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(M, fo, fi)) {
+      s = tc_gemm_forward(c->tc, c->stream, M, fo, fi, h, Wm, b, out, i < nl - 1);
+      c->launches += tc_gemm_launches(c->tc);
+      if (s) return fail(s, tc_gemm_error());
+    } else if (i < nl - 1) {
+      s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
+    } else {
+      s = sgemm<true, true, EPI_BIAS>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
+    }
+    if (s) return s;
+    h = out;
+  }
+  return HRP_OK;
+}
+
+// Backward over the first B rows (X rows [0,B), act rows [0,B)), dz [B][H] -> c->grad.
+hrp_status mlp_backward(hrp_ctx* c, int B) {
+  const int nl = (int)c->dims.size() - 1;
+  const float* dY = c->dz;
+  float* bufs[2] = {c->dh0, c->dh1};
+  int cur = 0;
+  for (int i = nl - 1; i >= 0; --i) {
+    const int fi = c->dims[i], fo = c->dims[i + 1];
+    const float* Hin = (i == 0) ? c->X : c->act[i - 1];
+    float* gW = c->grad + c->woff[i];
+    float* gb = gW + (int64_t)fi * fo;
+    // dW = dY^T . Hin  ([fo][fi]); reduction over the batch
+    hrp_status s = sgemm<false, false, EPI_STORE>(c, fo, fi, B, dY, fo, Hin, fi, gW, fi,
+                                                  nullptr, nullptr, 0);
+    if (s) return s;
+    colsum_kernel<<<(fo + 31) / 32, 256, 0, c->stream>>>(B, fo, dY, gb);
+    if ((s = launch_check(c))) return s;
+    if (i > 0) {
+      const float* Wm = c->theta + c->woff[i];
+      float* dH = bufs[cur];
+      s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
+      if (s) return s;
+      dY = dH;
+      cur ^= 1;
+    }
+  }
+  return HRP_OK;
+}
+
+hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
+  a.explicit_mode = c->explicit_mode;
+  a.n_evals = c->n_evals;
+  const int grid = std::min(a.M, c->sel_grid);
+  select_kernel<<<grid, kThreads, c->sel_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
+  return launch_check(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hrp_last_error(void) { return g_err.c_str(); }
+const char* hrp_version(void) { return "libhrp 0.1 (sm_100a)"; }
+
+hrp_status hrp_layout_table(const hrp_space* space, int32_t cap, int32_t* n_layouts,
+                            int32_t* layout_nslots, hrp_slot* slots, uint8_t* slot_type,
+                            int32_t* n_types, int64_t* n_actions) {
+  try {
+    HostSpace hs;
+    std::string err;
+    hrp_status s = build_space(space, hs, err);
+    if (s) return fail(s, err);
+    if (n_layouts) *n_layouts = hs.L;
+    if (n_types) *n_types = hs.T;
+    if (n_actions) *n_actions = hs.n_actions();
+    if (hs.L > cap) return fail(HRP_ERANGE, "cap smaller than the number of layouts");
+    for (int l = 0; l < hs.L; ++l) {
+      if (layout_nslots) layout_nslots[l] = hs.nslots[l];
+      for (int k = 0; k < 4; ++k) {
+        if (slots) slots[l * 4 + k] = k < hs.nslots[l] ? hs.slots[l][k] : hrp_slot{0, 0, 0};
+        if (slot_type) slot_type[l * 4 + k] = k < hs.nslots[l] ? hs.stype[l][k] : 255;
+      }
+    }
+    return HRP_OK;
+  } catch (const std::exception& e) {
+    return fail(HRP_ENOMEM, e.what());
+  }
+}
+
+hrp_status hrp_decode_action(const hrp_space* space, int64_t idx, int32_t* l, int32_t g[4],
+                             int32_t slot_of[4]) {
+  try {
+    HostSpace hs;
+    std::string err;
+    hrp_status s = build_space(space, hs, err);
+    if (s) return fail(s, err);
+    if (idx < 0 || idx >= hs.n_actions()) return fail(HRP_ERANGE, "action index out of range");
+    int lo = (int)(std::upper_bound(hs.off.begin(), hs.off.end(), idx) - hs.off.begin()) - 1;
+    const int C = hs.nslots[lo];
+    int64_t w = idx - hs.off[lo];
+    int64_t f = factorial(C);
+    int64_t rg = w / f, rs = w % f;
+    int v = 0;
+    for (int i = 0; i < 4; ++i) { g[i] = -1; slot_of[i] = -1; }
+    for (int i = 0; i < C; ++i) {
+      while (true) {
+        int64_t cc = binom(hs.W - 1 - v, C - 1 - i);
+        if (rg < cc) break;
+        rg -= cc;
+        ++v;
+      }
+      g[i] = v++;
+    }
+    std::vector<int> avail;
+    for (int i = 0; i < C; ++i) avail.push_back(i);
+    for (int i = 0; i < C; ++i) {
+      int64_t ff = factorial(C - 1 - i);
+      int d = (int)(rs / ff);
+      rs %= ff;
+      slot_of[i] = avail[d];
+      avail.erase(avail.begin() + d);
+    }
+    *l = lo;
+    return HRP_OK;
+  } catch (const std::exception& e) {
+    return fail(HRP_ENOMEM, e.what());
+  }
+}
+
+hrp_status hrp_nccl_unique_id(void* out) {
+  if (!out) return fail(HRP_EINVAL, "out is NULL");
+  ncclUniqueId id;
+  CKN(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return HRP_OK;
+}
+
+hrp_status hrp_env_destroy(hrp_ctx* c) {
+  if (!c) return HRP_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->tc) tc_gemm_destroy(c->tc);
+  c->ar.release();
+  delete c;
+  return HRP_OK;
+}
+
+hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
+                          const hrp_train_cfg* cfg, int device, void* cuda_stream, int rank,
+                          int world, const void* nccl_unique_id, const float* init_weights,
+                          hrp_ctx** out) {
+  if (!out) return fail(HRP_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(HRP_EINVAL, "cfg is NULL");
+  hrp_status s = validate_pool(prof);
+  if (s) return s;
+  if (world < 1 || rank < 0 || rank >= world) return fail(HRP_EINVAL, "bad rank/world");
+  if (world > 1 && !nccl_unique_id) return fail(HRP_EINVAL, "nccl_unique_id required for world > 1");
+  if (cfg->n_envs < 1 || cfg->batch < 1 || cfg->replay_capacity < cfg->batch)
+    return fail(HRP_ERANGE, "need n_envs >= 1, batch >= 1, replay_capacity >= batch");
+  if (cfg->n_envs > (1 << 24) || cfg->batch > (1 << 24) || cfg->replay_capacity > (1 << 28))
+    return fail(HRP_ERANGE, "n_envs / batch / replay_capacity too large");
+  if (cfg->hidden_layers < 1 || cfg->hidden_layers > 8 || cfg->hidden_width < 4 ||
+      cfg->hidden_width > 1024 || cfg->hidden_width % 4)
+    return fail(HRP_ERANGE, "hidden_layers 1..8, hidden_width 4..1024 multiple of 4");
+  if (!(cfg->lr >= 0.f) || !(cfg->gamma >= 0.f && cfg->gamma <= 1.f))
+    return fail(HRP_EINVAL, "lr >= 0 and 0 <= gamma <= 1 required");
+  std::unique_ptr<hrp_ctx> c(new hrp_ctx());
+  try {
+    std::string err;
+    s = build_space(space, c->hs, err);
+    if (s) return fail(s, err);
+  } catch (const std::exception& e) {
+    return fail(HRP_ENOMEM, e.what());
+  }
+  const HostSpace& hs = c->hs;
+  if (hs.L > 4096) return fail(HRP_ERANGE, "more than 4096 layouts");
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->rank = rank;
+  c->world = world;
+  c->cfg = *cfg;
+  CK(cudaSetDevice(device));
+  if ((s = init_constants(device))) return s;
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  // argmax mode: explicit enumeration of every action needs the group tables (W <= 16)
+  if (cfg->argmax_mode == 1 && hs.W > 16) return fail(HRP_ERANGE, "explicit argmax needs W <= 16");
+  c->explicit_mode = cfg->argmax_mode == 1 || (cfg->argmax_mode == 0 && hs.W <= 16);
+  c->gemm_mode = cfg->gemm_mode == 0 ? 2 : cfg->gemm_mode;
+  if ((s = upload_tables(hs, prof, c->explicit_mode, c->ar, c->stream, c->dt))) return s;
+  // network dims and flat parameter layout (W [out][in] then b [out] per layer)
+  c->dims.push_back(hs.W * kRowIn);
+  for (int i = 0; i < cfg->hidden_layers; ++i) c->dims.push_back(cfg->hidden_width);
+  c->dims.push_back(hs.head_width());
+  int64_t o = 0;
+  for (size_t i = 0; i + 1 < c->dims.size(); ++i) {
+    c->woff.push_back(o);
+    o += (int64_t)c->dims[i] * c->dims[i + 1] + c->dims[i + 1];
+  }
+  c->n_params = o;
+  const int E = cfg->n_envs, B = cfg->batch, W = hs.W, H = hs.head_width();
+  const int in = c->dims[0], wd = cfg->hidden_width;
+  c->rows_max = std::max({E, 2 * B, 8192});
+  const size_t R = c->rows_max;
+  Arena& ar = c->ar;
+  CK(ar.alloc((void**)&c->theta, sizeof(float) * o));
+  CK(ar.alloc((void**)&c->theta_t, sizeof(float) * o));
+  CK(ar.alloc((void**)&c->grad, sizeof(float) * o));
+  size_t ws = 0;
+  for (size_t i = 0; i + 1 < c->dims.size(); ++i)
+    ws = std::max(ws, (size_t)32 * c->dims[i] * c->dims[i + 1]);
+  c->ws_splitk_elems = ws;
+  CK(ar.alloc((void**)&c->ws_splitk, sizeof(float) * ws));
+  CK(ar.alloc((void**)&c->win, (size_t)E * W));
+  CK(ar.alloc((void**)&c->sched, sizeof(uint64_t) * E));
+  CK(cudaMemsetAsync(c->win, 0, (size_t)E * W, c->stream));
+  CK(cudaMemsetAsync(c->sched, 0, sizeof(uint64_t) * E, c->stream));
+  const size_t N = cfg->replay_capacity;
+  CK(ar.alloc((void**)&c->rep_win, N * W));
+  CK(ar.alloc((void**)&c->rep_sched, N * 8));
+  CK(ar.alloc((void**)&c->rep_act, N * 8));
+  CK(ar.alloc((void**)&c->rep_r, N * 4));
+  CK(ar.alloc((void**)&c->rep_done, N));
+  CK(ar.alloc((void**)&c->X, sizeof(float) * R * in));
+  for (int i = 0; i < cfg->hidden_layers; ++i) {
+    float* p;
+    CK(ar.alloc((void**)&p, sizeof(float) * R * wd));
+    c->act.push_back(p);
+  }
+  CK(ar.alloc((void**)&c->z, sizeof(float) * R * H));
+  CK(ar.alloc((void**)&c->zt, sizeof(float) * (size_t)B * H));
+  CK(ar.alloc((void**)&c->dz, sizeof(float) * (size_t)B * H));
+  CK(ar.alloc((void**)&c->dh0, sizeof(float) * (size_t)B * wd));
+  CK(ar.alloc((void**)&c->dh1, sizeof(float) * (size_t)B * wd));
+  CK(ar.alloc((void**)&c->bwin, R * W));
+  CK(ar.alloc((void**)&c->bsched, R * 8));
+  CK(ar.alloc((void**)&c->bact, R * 8));
+  CK(ar.alloc((void**)&c->br, R * 4));
+  CK(ar.alloc((void**)&c->bdone, R));
+  CK(ar.alloc((void**)&c->dsq, R * 4));
+  CK(ar.alloc((void**)&c->tmp_i64, R * 8));
+  CK(ar.alloc((void**)&c->n_evals, 8));
+  CK(cudaMemsetAsync(c->n_evals, 0, 8, c->stream));
+  if (init_weights) {
+    CK(cudaMemcpyAsync(c->theta, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->theta_t, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
+  } else {
+    CK(cudaMemsetAsync(c->theta, 0, sizeof(float) * o, c->stream));
+    CK(cudaMemsetAsync(c->theta_t, 0, sizeof(float) * o, c->stream));
+  }
+  // selection kernel launch shape
+  c->sel_smem = select_smem_bytes(hs.L, W, hs.T, H, hs.cmax, c->dt.sp.ncombo, c->explicit_mode);
+  if (c->sel_smem > 227 * 1024) return fail(HRP_ERANGE, "selection tables exceed shared memory");
+  CK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
+  CK(cudaFuncSetAttribute(td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
+  int occ = 1;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_kernel, kThreads, c->sel_smem));
+  c->sel_grid = nsm * std::max(1, occ);
+  if (c->gemm_mode == 2) {
+    if ((s = tc_gemm_create(&c->tc, device, (int)R, c->dims.data(), (int)c->dims.size()))) {
+      return fail(s, tc_gemm_error());
+    }
+  }
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    CKN(ncclCommInitRank(&c->comm, world, id, rank));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  *out = c.release();
+  return HRP_OK;
+}
+
+hrp_status hrp_env_reset(hrp_ctx* c, const uint8_t* d_windows) {
+  if (!c || !d_windows) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->win, d_windows, (size_t)c->cfg.n_envs * c->hs.W, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->sched, 0, sizeof(uint64_t) * c->cfg.n_envs, c->stream));
+  return HRP_OK;
+}
+
+hrp_status hrp_env_step(hrp_ctx* c, uint64_t thr, const uint32_t* d_u_explore,
+                        const uint64_t* d_u_action, const uint8_t* d_next_windows,
+                        int64_t* d_actions, float* d_rewards, uint8_t* d_done, int64_t* d_corun,
+                        float* d_qsel, int64_t* d_greedy) {
+  if (!c || !d_u_explore || !d_u_action || !d_next_windows || !d_actions || !d_rewards || !d_done)
+    return fail(HRP_EINVAL, "NULL argument");
+  if (thr > (1ull << 32)) return fail(HRP_EINVAL, "eps_threshold must be <= 2^32");
+  CK(cudaSetDevice(c->device));
+  const int E = c->cfg.n_envs;
+  hrp_status s;
+  encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool, c->X);
+  if ((s = launch_check(c))) return s;
+  if ((s = mlp_forward(c, c->theta, c->X, E, c->z))) return s;
+  SelArgs a{};
+  a.M = E;
+  a.z = c->z;
+  a.mode = SEL_STEP;
+  a.win = c->win;
+  a.sched = c->sched;
+  a.thr = thr;
+  a.u_explore = d_u_explore;
+  a.u_action = d_u_action;
+  a.next_win = d_next_windows;
+  a.lam = c->cfg.reward_lambda;
+  a.actions = d_actions;
+  a.rewards = d_rewards;
+  a.done = d_done;
+  a.corun = d_corun;
+  a.qsel = d_qsel;
+  a.greedy = d_greedy;
+  a.rep_win = c->rep_win;
+  a.rep_sched = c->rep_sched;
+  a.rep_act = c->rep_act;
+  a.rep_r = c->rep_r;
+  a.rep_done = c->rep_done;
+  a.t_step = c->t;
+  a.N_rep = c->cfg.replay_capacity;
+  if ((s = launch_select(c, a))) return s;
+  c->t += 1;
+  c->inserted += E;
+  return HRP_OK;
+}
+
+hrp_status hrp_q_forward(hrp_ctx* c, int64_t n, const uint8_t* d_windows, const uint64_t* d_sched,
+                         int64_t* d_argmax, float* d_qmax, float* d_head) {
+  if (!c || !d_windows || !d_sched || !d_argmax || !d_qmax) return fail(HRP_EINVAL, "NULL argument");
+  if (n < 0) return fail(HRP_EINVAL, "n < 0");
+  CK(cudaSetDevice(c->device));
+  const int W = c->hs.W, H = c->hs.head_width();
+  hrp_status s;
+  for (int64_t r0 = 0; r0 < n; r0 += c->rows_max) {
+    const int M = (int)std::min<int64_t>(c->rows_max, n - r0);
+    const uint8_t* wp = d_windows + r0 * W;
+    const uint64_t* sp = d_sched + r0;
+    encode_kernel<<<(M + 7) / 8, 256, 0, c->stream>>>(M, W, wp, sp, c->dt.pool, c->X);
+    if ((s = launch_check(c))) return s;
+    float* zo = d_head ? d_head + r0 * H : c->z;
+    if ((s = mlp_forward(c, c->theta, c->X, M, zo))) return s;
+    SelArgs a{};
+    a.M = M;
+    a.z = zo;
+    a.mode = SEL_INFER;
+    a.win = const_cast<uint8_t*>(wp);
+    a.sched = const_cast<uint64_t*>(sp);
+    a.actions = d_argmax + r0;
+    a.qmax = d_qmax + r0;
+    if ((s = launch_select(c, a))) return s;
+  }
+  return HRP_OK;
+}
+
+hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_target, float* d_loss,
+                          int64_t* d_sample_idx, int64_t* d_astar) {
+  if (!c || !d_u_replay || !d_loss) return fail(HRP_EINVAL, "NULL argument");
+  const int B = c->cfg.batch;
+  if (c->inserted < B) return fail(HRP_ESTATE, "replay holds fewer than batch transitions");
+  CK(cudaSetDevice(c->device));
+  const int64_t nf = std::min<int64_t>(c->cfg.replay_capacity, c->inserted);
+  const int H = c->hs.head_width();
+  hrp_status s;
+  sample_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(
+      c->dt.sp, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r, c->rep_done,
+      c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx);
+  if ((s = launch_check(c))) return s;
+  encode_kernel<<<(2 * B + 7) / 8, 256, 0, c->stream>>>(2 * B, c->hs.W, c->bwin, c->bsched,
+                                                         c->dt.pool, c->X);
+  if ((s = launch_check(c))) return s;
+  // online net on [s; s'] (activations of the s rows kept for backward), target on s'
+  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z))) return s;
+  // target forward reuses act buffers rows [B,2B) scratch: run on X rows [B,2B) into zt
+  {
+    // hidden activations of the target pass must not clobber rows [0,B) kept for backward:
+    // the act buffers hold 2B rows; point the target pass at rows [B, 2B).
+    std::vector<float*> saved = c->act;
+    for (auto& p : c->act) p += (size_t)B * c->cfg.hidden_width;
+    s = mlp_forward(c, c->theta_t, c->X + (size_t)B * c->dims[0], B, c->zt);
+    c->act = saved;
+    if (s) return s;
+  }
+  TdArgs t{};
+  t.B = B;
+  t.z_all = c->z;
+  t.z_tgt = c->zt;
+  t.bsched = c->bsched;
+  t.bact = c->bact;
+  t.br = c->br;
+  t.bdone = c->bdone;
+  t.gamma = c->cfg.gamma;
+  t.inv_btot = 1.f / ((float)B * (float)c->world);
+  t.explicit_mode = c->explicit_mode;
+  t.dz = c->dz;
+  t.dsq = c->dsq;
+  t.astar = d_astar;
+  t.n_evals = c->n_evals;
+  td_kernel<<<std::min(B, c->sel_grid), kThreads, c->sel_smem, c->stream>>>(c->dt.sp, t);
+  if ((s = launch_check(c))) return s;
+  loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
+  if ((s = launch_check(c))) return s;
+  if ((s = mlp_backward(c, B))) return s;
+  if (c->world > 1) {
+    CKN(ncclAllReduce(c->grad, c->grad, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, c->stream));
+  }
+  sgd_kernel<<<4 * 148, 256, 0, c->stream>>>(c->n_params, c->cfg.lr, c->theta, c->grad, c->theta_t,
+                                              sync_target);
+  if ((s = launch_check(c))) return s;
+  (void)H;
+  return HRP_OK;
+}
+
+hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* prof, int64_t n,
+                                  const uint8_t* d_windows, int64_t* d_best, int64_t* d_solo,
+                                  uint8_t* d_rgs, int64_t* d_bact, void* cuda_stream) {
+  if (!d_windows || !d_best || !d_solo || !d_rgs || !d_bact) return fail(HRP_EINVAL, "NULL argument");
+  if (n < 0) return fail(HRP_EINVAL, "n < 0");
+  hrp_status s = validate_pool(prof);
+  if (s) return s;
+  HostSpace hs;
+  try {
+    std::string err;
+    if ((s = build_space(space, hs, err))) return fail(s, err);
+  } catch (const std::exception& e) {
+    return fail(HRP_ENOMEM, e.what());
+  }
+  if (hs.W > kBruteMaxW) return fail(HRP_ERANGE, "brute force supports W <= 12");
+  if (hs.L > 512) return fail(HRP_ERANGE, "brute force supports <= 512 layouts");
+  if (hs.n_actions() >= (int64_t(1) << kBruteIdxBits)) return fail(HRP_ERANGE, "|A| >= 2^26");
+  if (n == 0) return HRP_OK;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if ((s = init_constants(dev))) return s;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  Arena ar;
+  DevTables dt;
+  if ((s = upload_tables(hs, prof, true, ar, st, dt))) { ar.release(); return s; }
+  const size_t smem = brute_smem_bytes(hs.W, hs.L, hs.T);
+  cudaError_t e = cudaFuncSetAttribute(brute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { ar.release(); return fail(HRP_ECUDA, cudaGetErrorString(e)); }
+  int nsm = 148, occ = 1;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brute_kernel, 512, smem);
+  const int grid = (int)std::min<int64_t>(n, (int64_t)nsm * std::max(1, occ));
+  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact};
+  brute_kernel<<<grid, 512, smem, st>>>(dt.sp, dt.pool, a);
+  e = cudaGetLastError();
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  ar.release();
+  if (e != cudaSuccess) return fail(HRP_ECUDA, cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(HRP_ECUDA, cudaGetErrorString(e2));
+  return HRP_OK;
+}
+
+int64_t hrp_n_params(const hrp_ctx* c) { return c ? c->n_params : -1; }
+int32_t hrp_head_width(const hrp_ctx* c) { return c ? c->hs.head_width() : -1; }
+int64_t hrp_launch_count(const hrp_ctx* c) { return c ? c->launches : -1; }
+
+hrp_status hrp_get_weights(hrp_ctx* c, float* out) {
+  if (!c || !out) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(out, c->theta, sizeof(float) * c->n_params, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(out + c->n_params, c->theta_t, sizeof(float) * c->n_params, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return HRP_OK;
+}
+
+hrp_status hrp_set_weights(hrp_ctx* c, const float* in) {
+  if (!c || !in) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->theta, in, sizeof(float) * c->n_params, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->theta_t, in + c->n_params, sizeof(float) * c->n_params, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return HRP_OK;
+}
+
+hrp_status hrp_sync(hrp_ctx* c) {
+  if (!c) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->comm) {
+    ncclResult_t r;
+    CKN(ncclCommGetAsyncError(c->comm, &r));
+    if (r != ncclSuccess) return fail(HRP_ENCCL, ncclGetErrorString(r));
+  }
+  return HRP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+"""GPU parity: hrp_bruteforce_optimum (a14) vs the oracle's subset DP -- bit-exact.
+
+The oracle's DP is itself pinned to the RGS enumeration and the literal search
+(tests/test_oracle_pruned_brute.py)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import brute as BR
+from oracle import space as SP
+from synth.configs import SpaceCfg
+
+pytestmark = pytest.mark.gpu
+S10 = tuple(range(10, 100, 10))
+
+
+def _cmp(scfg, pool, wins):
+    from paper_2405_08754_b200.session import bruteforce
+    best, solo, rgs, bact = bruteforce(scfg, pool, wins)
+    sp = SP.build_space(scfg.window, scfg.cmax, scfg.shares, scfg.mig)
+    for i, w in enumerate(wins):
+        ref = BR.dp_opt(sp, [int(x) for x in w], pool, scfg.interference_q3)
+        assert best[i] == ref["cost"], i
+        assert solo[i] == ref["solo"], i
+        assert list(rgs[i]) == ref["rgs"], i
+        assert list(bact[i]) == ref["block_action"], i
+
+
+@pytest.mark.parametrize("W,cmax,S,mig", [(3, 2, (25, 50, 75), True), (5, 3, (25, 50, 75), True),
+                                          (6, 4, (50,), True), (7, 3, S10, False),
+                                          (8, 2, S10, True), (1, 1, (50,), True)])
+def test_small_spaces(W, cmax, S, mig):
+    pool = synth.make_pool(27)
+    scfg = SpaceCfg(W, cmax, S, mig)
+    wins = synth.make_windows(pool, 24, W, step=W * 10 + cmax)
+    _cmp(scfg, pool, wins)
+
+
+def test_heavy_ties():
+    from types import SimpleNamespace
+    T = np.array([1000, 1000, 2000, 4000], np.int64)
+    pool = SimpleNamespace(solo_ticks=T, compute_pm=np.full(4, 100, np.int16),
+                           memory_pm=np.full(4, 100, np.int16),
+                           features=np.zeros((4, 12), np.float32))
+    rng = np.random.default_rng(9)
+    wins = rng.integers(0, 4, (16, 8)).astype(np.uint8)
+    _cmp(SpaceCfg(8, 4, (25, 50, 75)), pool, wins)
+
+
+def test_config3_table_v_and_random():
+    # config 3: W = 12, Cmax = 4, Q1-Q12 of Table V + random class-stratified windows
+    pool = synth.make_pool(27)
+    scfg = synth.config(3).space
+    wins = np.concatenate([synth.table_v_windows(pool),
+                           synth.make_windows(pool, 8, 12, step=77)])
+    _cmp(scfg, pool, wins)
+
+
+def test_config3_full_launch_sampled():
+    # the bench's launch: Q1-Q12 + 4096 windows in one call; oracle checks a sample
+    from paper_2405_08754_b200.session import bruteforce
+    pool = synth.make_pool(27)
+    scfg = synth.config(3).space
+    wins = np.concatenate([synth.table_v_windows(pool),
+                           synth.make_windows(pool, 4096, 12, step=1)])
+    best, solo, rgs, bact = bruteforce(scfg, pool, wins)
+    assert (best <= solo).all() and (best > 0).all()
+    sp = SP.build_space(12, 4, S10)
+    for i in (0, 11, 12, 1000, 2047, 4107):
+        ref = BR.dp_opt(sp, [int(x) for x in wins[i]], pool)
+        assert (best[i], solo[i], list(rgs[i]), list(bact[i])) == \
+            (ref["cost"], ref["solo"], ref["rgs"], ref["block_action"])
