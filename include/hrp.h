@@ -183,6 +183,26 @@ hrp_status hrp_get_weights(hrp_ctx *ctx, float *out);
 hrp_status hrp_set_weights(hrp_ctx *ctx, const float *in /*[2 * n_params]*/);
 /* Number of libhrp kernel launches enqueued so far by this context (for bench.py). */
 int64_t hrp_launch_count(const hrp_ctx *ctx);
+/* Per-kernel device timing: with profiling enabled every libhrp launch on the context's
+ * stream is bracketed by CUDA events; hrp_profile_read synchronises and returns the summed
+ * milliseconds and launch counts per kernel class (arrays of HRP_K_COUNT, host). */
+typedef enum {
+  HRP_K_ENCODE = 0,   /* a2 state encoding                                          */
+  HRP_K_GEMM_FWD = 1, /* a3 Q-MLP forward GEMMs (+ fused bias / ReLU)                */
+  HRP_K_GEMM_BWD = 2, /* a11 backward GEMMs, split-K reduce, bias column sums         */
+  HRP_K_SELECT = 3,   /* a4-a7 fused centering / argmax / epsilon / reward / replay   */
+  HRP_K_TD = 4,       /* a9-a10 double-DQN target argmax, TD error, head gradient     */
+  HRP_K_SAMPLE = 5,   /* a8 replay sample                                            */
+  HRP_K_SGD = 6,      /* a13 SGD + target sync                                        */
+  HRP_K_MISC = 7,     /* loss reduction                                             */
+  HRP_K_ALLREDUCE = 8,/* a12 NCCL gradient allreduce (world > 1)                      */
+  HRP_K_COUNT = 9
+} hrp_kernel_class;
+hrp_status hrp_profile(hrp_ctx *ctx, int enable); /* 1: clear + start recording; 0: stop */
+hrp_status hrp_profile_read(hrp_ctx *ctx, double *ms, int64_t *launches);
+/* Explicit Q^ evaluations (valid (l, g, sigma) scored; pruned mode: candidate assignments)
+ * counted by the selection kernels since create (synchronises the stream). */
+int64_t hrp_eval_count(hrp_ctx *ctx);
 /* Block until the context's stream is idle; returns any pending CUDA/NCCL error. */
 hrp_status hrp_sync(hrp_ctx *ctx);
 const char *hrp_last_error(void);

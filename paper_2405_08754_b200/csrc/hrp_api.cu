@@ -241,14 +241,47 @@ struct hrp_ctx {
   int sel_grid = 0;
   int64_t launches = 0;
   TcGemm* tc = nullptr;
+  // per-kernel device timing (hrp_profile)
+  bool prof = false;
+  int gemm_cls = HRP_K_GEMM_FWD;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t ev_begin = nullptr;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_rec;
 };
 
 namespace {
 
-hrp_status launch_check(hrp_ctx* c) {
+cudaEvent_t prof_event(hrp_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    if (c->ev_pool.size() >= 200000) return nullptr;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+// Record the start of a launch (only when profiling).
+void prof_begin(hrp_ctx* c) {
+  c->ev_begin = nullptr;
+  if (!c->prof) return;
+  c->ev_begin = prof_event(c);
+  if (c->ev_begin) cudaEventRecord(c->ev_begin, c->stream);
+}
+
+hrp_status launch_check(hrp_ctx* c, int cls) {
   c->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HRP_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  if (c->prof && c->ev_begin) {
+    cudaEvent_t end = prof_event(c);
+    if (end) {
+      cudaEventRecord(end, c->stream);
+      c->prof_rec.push_back({cls, {c->ev_begin, end}});
+    }
+    c->ev_begin = nullptr;
+  }
   return HRP_OK;
 }
 
@@ -259,16 +292,18 @@ hrp_status sgemm(hrp_ctx* c, int M, int N, int K, const float* A, int lda, const
   const int64_t t128 = (int64_t)((M + 127) / 128) * ((N + 127) / 128);
   if (EPI != EPI_STORE && t128 >= 2 * 148) {
     dim3 grid((N + 127) / 128, (M + 127) / 128, 1);
+    prof_begin(c);
     sgemm_kernel<128, 128, 8, 8, AK, BKc, EPI><<<grid, 256, 0, c->stream>>>(
         M, N, K, A, lda, B, ldb, C, ldc, bias, aux, ldaux, K);
-    return launch_check(c);
+    return launch_check(c, c->gemm_cls);
   }
   const int64_t t64 = (int64_t)((M + 63) / 64) * ((N + 63) / 64);
   if (EPI != EPI_STORE) {
     dim3 grid((N + 63) / 64, (M + 63) / 64, 1);
+    prof_begin(c);
     sgemm_kernel<64, 64, 4, 4, AK, BKc, EPI><<<grid, 256, 0, c->stream>>>(
         M, N, K, A, lda, B, ldb, C, ldc, bias, aux, ldaux, K);
-    return launch_check(c);
+    return launch_check(c, c->gemm_cls);
   }
   // split-K into the workspace, then a deterministic reduce into C (ldc == N)
   int S = (int)std::min<int64_t>(32, std::max<int64_t>(1, (2 * 148 + t64 - 1) / t64));
@@ -277,19 +312,22 @@ hrp_status sgemm(hrp_ctx* c, int M, int N, int K, const float* A, int lda, const
   S = (K + kc - 1) / kc;
   if ((size_t)S * M * N > c->ws_splitk_elems) return fail(HRP_ENOMEM, "split-K workspace too small");
   dim3 grid((N + 63) / 64, (M + 63) / 64, S);
+  prof_begin(c);
   sgemm_kernel<64, 64, 4, 4, AK, BKc, EPI_STORE><<<grid, 256, 0, c->stream>>>(
       M, N, K, A, lda, B, ldb, c->ws_splitk, N, bias, aux, ldaux, kc);
-  hrp_status s = launch_check(c);
+  hrp_status s = launch_check(c, c->gemm_cls);
   if (s) return s;
   const int64_t n = (int64_t)M * N;
+  prof_begin(c);
   splitk_reduce_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(
       S, n, c->ws_splitk, C);
-  return launch_check(c);
+  return launch_check(c, c->gemm_cls);
 }
 
 // Forward of one network over M rows of X.  If keep, hidden outputs go to c->act (for the
 // backward pass); z_out [M][H].
 hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out) {
+  c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
   const float* h = X;
   for (int i = 0; i < nl; ++i) {
@@ -299,9 +337,11 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, fl
     float* out = (i == nl - 1) ? z_out : c->act[i];
     hrp_status s;
     if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(M, fo, fi)) {
+      prof_begin(c);
       s = tc_gemm_forward(c->tc, c->stream, M, fo, fi, h, Wm, b, out, i < nl - 1);
-      c->launches += tc_gemm_launches(c->tc);
       if (s) return fail(s, tc_gemm_error());
+      c->launches += tc_gemm_launches(c->tc) - 1;
+      if ((s = launch_check(c, HRP_K_GEMM_FWD))) return s;
     } else if (i < nl - 1) {
       s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
     } else {
@@ -315,6 +355,7 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, fl
 
 // Backward over the first B rows (X rows [0,B), act rows [0,B)), dz [B][H] -> c->grad.
 hrp_status mlp_backward(hrp_ctx* c, int B) {
+  c->gemm_cls = HRP_K_GEMM_BWD;
   const int nl = (int)c->dims.size() - 1;
   const float* dY = c->dz;
   float* bufs[2] = {c->dh0, c->dh1};
@@ -328,8 +369,9 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     hrp_status s = sgemm<false, false, EPI_STORE>(c, fo, fi, B, dY, fo, Hin, fi, gW, fi,
                                                   nullptr, nullptr, 0);
     if (s) return s;
+    prof_begin(c);
     colsum_kernel<<<(fo + 31) / 32, 256, 0, c->stream>>>(B, fo, dY, gb);
-    if ((s = launch_check(c))) return s;
+    if ((s = launch_check(c, HRP_K_GEMM_BWD))) return s;
     if (i > 0) {
       const float* Wm = c->theta + c->woff[i];
       float* dH = bufs[cur];
@@ -346,8 +388,9 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.explicit_mode = c->explicit_mode;
   a.n_evals = c->n_evals;
   const int grid = std::min(a.M, c->sel_grid);
+  prof_begin(c);
   select_kernel<<<grid, kThreads, c->sel_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
-  return launch_check(c);
+  return launch_check(c, HRP_K_SELECT);
 }
 
 }  // namespace
@@ -436,6 +479,7 @@ hrp_status hrp_env_destroy(hrp_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->tc) tc_gemm_destroy(c->tc);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   c->ar.release();
   delete c;
   return HRP_OK;
@@ -548,8 +592,16 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   // selection kernel launch shape
   c->sel_smem = select_smem_bytes(hs.L, W, hs.T, H, hs.cmax, c->dt.sp.ncombo, c->explicit_mode);
   if (c->sel_smem > 227 * 1024) return fail(HRP_ERANGE, "selection tables exceed shared memory");
-  CK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
-  CK(cudaFuncSetAttribute(td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
+  {
+    // the attribute is per function (process-wide): keep the largest any context needs
+    static int sel_smem_max[64] = {0};
+    int& mx = sel_smem_max[device & 63];
+    if ((int)c->sel_smem > mx) {
+      CK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
+      CK(cudaFuncSetAttribute(td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
+      mx = (int)c->sel_smem;
+    }
+  }
   int occ = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_kernel, kThreads, c->sel_smem));
   c->sel_grid = nsm * std::max(1, occ);
@@ -586,8 +638,9 @@ hrp_status hrp_env_step(hrp_ctx* c, uint64_t thr, const uint32_t* d_u_explore,
   CK(cudaSetDevice(c->device));
   const int E = c->cfg.n_envs;
   hrp_status s;
+  prof_begin(c);
   encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool, c->X);
-  if ((s = launch_check(c))) return s;
+  if ((s = launch_check(c, HRP_K_ENCODE))) return s;
   if ((s = mlp_forward(c, c->theta, c->X, E, c->z))) return s;
   SelArgs a{};
   a.M = E;
@@ -630,8 +683,9 @@ hrp_status hrp_q_forward(hrp_ctx* c, int64_t n, const uint8_t* d_windows, const 
     const int M = (int)std::min<int64_t>(c->rows_max, n - r0);
     const uint8_t* wp = d_windows + r0 * W;
     const uint64_t* sp = d_sched + r0;
+    prof_begin(c);
     encode_kernel<<<(M + 7) / 8, 256, 0, c->stream>>>(M, W, wp, sp, c->dt.pool, c->X);
-    if ((s = launch_check(c))) return s;
+    if ((s = launch_check(c, HRP_K_ENCODE))) return s;
     float* zo = d_head ? d_head + r0 * H : c->z;
     if ((s = mlp_forward(c, c->theta, c->X, M, zo))) return s;
     SelArgs a{};
@@ -656,13 +710,15 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   const int64_t nf = std::min<int64_t>(c->cfg.replay_capacity, c->inserted);
   const int H = c->hs.head_width();
   hrp_status s;
+  prof_begin(c);
   sample_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(
       c->dt.sp, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r, c->rep_done,
       c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx);
-  if ((s = launch_check(c))) return s;
+  if ((s = launch_check(c, HRP_K_SAMPLE))) return s;
+  prof_begin(c);
   encode_kernel<<<(2 * B + 7) / 8, 256, 0, c->stream>>>(2 * B, c->hs.W, c->bwin, c->bsched,
                                                          c->dt.pool, c->X);
-  if ((s = launch_check(c))) return s;
+  if ((s = launch_check(c, HRP_K_ENCODE))) return s;
   // online net on [s; s'] (activations of the s rows kept for backward), target on s'
   if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z))) return s;
   // target forward reuses act buffers rows [B,2B) scratch: run on X rows [B,2B) into zt
@@ -690,17 +746,23 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.dsq = c->dsq;
   t.astar = d_astar;
   t.n_evals = c->n_evals;
+  prof_begin(c);
   td_kernel<<<std::min(B, c->sel_grid), kThreads, c->sel_smem, c->stream>>>(c->dt.sp, t);
-  if ((s = launch_check(c))) return s;
+  if ((s = launch_check(c, HRP_K_TD))) return s;
+  prof_begin(c);
   loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
-  if ((s = launch_check(c))) return s;
+  if ((s = launch_check(c, HRP_K_MISC))) return s;
   if ((s = mlp_backward(c, B))) return s;
   if (c->world > 1) {
+    prof_begin(c);
     CKN(ncclAllReduce(c->grad, c->grad, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, c->stream));
+    c->launches--;  // NCCL's kernel, not ours
+    if ((s = launch_check(c, HRP_K_ALLREDUCE))) return s;
   }
+  prof_begin(c);
   sgd_kernel<<<4 * 148, 256, 0, c->stream>>>(c->n_params, c->cfg.lr, c->theta, c->grad, c->theta_t,
                                               sync_target);
-  if ((s = launch_check(c))) return s;
+  if ((s = launch_check(c, HRP_K_SGD))) return s;
   (void)H;
   return HRP_OK;
 }
@@ -731,7 +793,12 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   DevTables dt;
   if ((s = upload_tables(hs, prof, true, ar, st, dt))) { ar.release(); return s; }
   const size_t smem = brute_smem_bytes(hs.W, hs.L, hs.T);
-  cudaError_t e = cudaFuncSetAttribute(brute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static int brute_smem_max[64] = {0};
+  cudaError_t e = cudaSuccess;
+  if ((int)smem > brute_smem_max[dev & 63]) {
+    e = cudaFuncSetAttribute(brute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) brute_smem_max[dev & 63] = (int)smem;
+  }
   if (e != cudaSuccess) { ar.release(); return fail(HRP_ECUDA, cudaGetErrorString(e)); }
   int nsm = 148, occ = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -745,6 +812,38 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   if (e != cudaSuccess) return fail(HRP_ECUDA, cudaGetErrorString(e));
   if (e2 != cudaSuccess) return fail(HRP_ECUDA, cudaGetErrorString(e2));
   return HRP_OK;
+}
+
+hrp_status hrp_profile(hrp_ctx* c, int enable) {
+  if (!c) return fail(HRP_EINVAL, "NULL argument");
+  if (enable) {
+    c->prof_rec.clear();
+    c->ev_used = 0;
+  }
+  c->prof = enable != 0;
+  return HRP_OK;
+}
+
+hrp_status hrp_profile_read(hrp_ctx* c, double* ms, int64_t* count) {
+  if (!c || !ms || !count) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < HRP_K_COUNT; ++k) { ms[k] = 0.0; count[k] = 0; }
+  for (auto& r : c->prof_rec) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.second.first, r.second.second));
+    ms[r.first] += t;
+    count[r.first] += 1;
+  }
+  return HRP_OK;
+}
+
+int64_t hrp_eval_count(hrp_ctx* c) {
+  if (!c) return -1;
+  unsigned long long v = 0;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return -1;
+  if (cudaMemcpy(&v, c->n_evals, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return (int64_t)v;
 }
 
 int64_t hrp_n_params(const hrp_ctx* c) { return c ? c->n_params : -1; }

@@ -144,14 +144,20 @@ __device__ inline void load_tabs(const DevSpace& sp, SelSmem& s, bool explicit_m
         s.t.cmem[C][i] = sp.combo[C][i];
       }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  // every thread needs cstart (SelSmem is per-thread); nlay_c comes with the space
+  {
     int k = 0;
     for (int C = 1; C <= 4; ++C) {
       s.t.cstart[C] = k;
-      for (int l = 0; l < sp.L; ++l)
-        if (s.t.nsl[l] == C) s.t.lay_of_c[k++] = (uint16_t)l;
+      k += sp.nlay_c[C];
     }
     s.t.cstart[5] = k;
+  }
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int C = 1; C <= 4; ++C)
+      for (int l = 0; l < sp.L; ++l)
+        if (s.t.nsl[l] == C) s.t.lay_of_c[k++] = (uint16_t)l;
   }
   __syncthreads();
 }

@@ -71,13 +71,15 @@ def lib():
             "hrp_get_weights": [P, P],
             "hrp_set_weights": [P, P],
             "hrp_sync": [P],
+            "hrp_profile": [P, S],
+            "hrp_profile_read": [P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
             f.argtypes = args
             f.restype = C.c_int
         for name, rt in (("hrp_n_params", C.c_int64), ("hrp_head_width", C.c_int32),
-                         ("hrp_launch_count", C.c_int64)):
+                         ("hrp_launch_count", C.c_int64), ("hrp_eval_count", C.c_int64)):
             getattr(L, name).argtypes = [P]
             getattr(L, name).restype = rt
         L.hrp_last_error.restype = C.c_char_p
@@ -234,6 +236,25 @@ def hrp_get_weights(ctx):
 def hrp_set_weights(ctx, w):
     w = np.ascontiguousarray(w, np.float32)
     _check(lib().hrp_set_weights(ctx, _hptr(w)))
+
+
+KERNEL_CLASSES = ["encode", "gemm_fwd", "gemm_bwd", "select", "td", "sample", "sgd", "misc",
+                  "allreduce"]
+
+
+def hrp_profile(ctx, enable):
+    _check(lib().hrp_profile(ctx, int(bool(enable))))
+
+
+def hrp_profile_read(ctx):
+    ms = np.zeros(len(KERNEL_CLASSES), np.float64)
+    cnt = np.zeros(len(KERNEL_CLASSES), np.int64)
+    _check(lib().hrp_profile_read(ctx, _hptr(ms), _hptr(cnt)))
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}
+
+
+def hrp_eval_count(ctx):
+    return lib().hrp_eval_count(ctx)
 
 
 def hrp_sync(ctx):
