@@ -1,16 +1,23 @@
-// tcgen05 (5th-gen tensor core) GEMM for the Q-MLP layers: Y = act(X . W^T + b) in 3xTF32
-// (split hi/lo operands, fp32 accumulate in TMEM).  Internal interface.
+// tcgen05 (5th-gen tensor core) GEMM for the Q-MLP layers: D = epi(A . B^T) in 3xTF32
+// (activation operand split hi/lo in shared memory, weights pre-split), fp32 accumulate in
+// TMEM.  Internal interface of libhrp.
 #pragma once
 #include <cuda_runtime.h>
 #include "../../include/hrp.h"
 
 namespace hrp {
 struct TcGemm;
+enum { TC_EPI_BIAS = 0, TC_EPI_BIAS_RELU = 1, TC_EPI_RELU_MASK = 2 };
 hrp_status tc_gemm_create(TcGemm** out, int device, int rows_max, const int* dims, int ndims);
 void tc_gemm_destroy(TcGemm* g);
 bool tc_gemm_supported(int M, int N, int K);
-hrp_status tc_gemm_forward(TcGemm* g, cudaStream_t st, int M, int N, int K, const float* X,
-                           const float* Wt, const float* b, float* Y, bool relu);
+// A [M][K] fp32 row-major; Bh/Bl [N][K] hi/lo split; D [M][N]; aux [M][ldaux] (ReLU mask).
+hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, const float* A,
+                       const float* Bh, const float* Bl, const float* bias, const float* aux,
+                       int ldaux, float* D);
+// hi/lo split of W [rows][cols]; optionally also of W^T ([cols][rows]) into hiT/loT.
+hrp_status tc_split(TcGemm* g, cudaStream_t st, int rows, int cols, const float* w, float* hi,
+                    float* lo, float* hiT, float* loT);
 int tc_gemm_launches(TcGemm* g);
 const char* tc_gemm_error();
 }  // namespace hrp

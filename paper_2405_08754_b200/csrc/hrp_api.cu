@@ -17,6 +17,7 @@
 #include "k_gemm_simt.cuh"
 #include "k_env.cuh"
 #include "k_brute.cuh"
+#include "k_pruned.cuh"
 #include "gemm_tc.h"
 
 using namespace hrp;
@@ -210,6 +211,9 @@ struct hrp_ctx {
   std::vector<int64_t> woff; // per layer offset of W in the flat params
   int64_t n_params = 0;
   float *theta = nullptr, *theta_t = nullptr, *grad = nullptr, *ws_splitk = nullptr;
+  // 3xTF32 operand splits for the tcgen05 GEMMs: [online hi | online lo | target hi | target lo]
+  // in the flat parameter layout, and the online weights transposed ([in][out]) hi | lo.
+  float *wsplit = nullptr, *wsplitT = nullptr;
   size_t ws_splitk_elems = 0;
   // env state
   uint8_t* win = nullptr;
@@ -238,6 +242,8 @@ struct hrp_ctx {
   int64_t* tmp_i64 = nullptr;         // [rows]
   unsigned long long* n_evals = nullptr;
   size_t sel_smem = 0;
+  size_t p_smem = 0;   // pruned warp-per-state kernels
+  int p_grid = 0;
   int sel_grid = 0;
   int64_t launches = 0;
   TcGemm* tc = nullptr;
@@ -324,11 +330,44 @@ hrp_status sgemm(hrp_ctx* c, int M, int N, int K, const float* A, int lda, const
   return launch_check(c, c->gemm_cls);
 }
 
-// Forward of one network over M rows of X.  If keep, hidden outputs go to c->act (for the
-// backward pass); z_out [M][H].
+// 3xTF32 hi/lo splits of the online (and transposed online) or target weights.
+hrp_status split_weights(hrp_ctx* c, bool target) {
+  if (!c->tc) return HRP_OK;
+  const int nl = (int)c->dims.size() - 1;
+  const float* th = target ? c->theta_t : c->theta;
+  float* hi = c->wsplit + (target ? 2 : 0) * c->n_params;
+  float* lo = hi + c->n_params;
+  for (int i = 0; i < nl; ++i) {
+    const int fi = c->dims[i], fo = c->dims[i + 1];
+    const int64_t o = c->woff[i];
+    float* hT = target ? nullptr : c->wsplitT + o;
+    float* lT = target ? nullptr : c->wsplitT + c->n_params + o;
+    prof_begin(c);
+    hrp_status s = tc_split(c->tc, c->stream, fo, fi, th + o, hi + o, lo + o, hT, lT);
+    if (s) return fail(s, tc_gemm_error());
+    c->launches += tc_gemm_launches(c->tc) - 1;
+    if ((s = launch_check(c, HRP_K_SGD))) return s;
+  }
+  return HRP_OK;
+}
+
+// Tensor-core GEMM D = epi(A . B^T) with pre-split B (hi, lo).
+hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, const float* A,
+                  const float* Bh, const float* Bl, const float* bias, const float* aux, int ldaux,
+                  float* D) {
+  prof_begin(c);
+  hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
+  if (s) return fail(s, tc_gemm_error());
+  c->launches += tc_gemm_launches(c->tc) - 1;
+  return launch_check(c, cls);
+}
+
+// Forward of one network over M rows of X: hidden outputs to c->act (kept for the backward
+// pass), head output z_out [M][H].
 hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out) {
   c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
+  const bool target = theta == c->theta_t;
   const float* h = X;
   for (int i = 0; i < nl; ++i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
@@ -337,11 +376,9 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, fl
     float* out = (i == nl - 1) ? z_out : c->act[i];
     hrp_status s;
     if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(M, fo, fi)) {
-      prof_begin(c);
-      s = tc_gemm_forward(c->tc, c->stream, M, fo, fi, h, Wm, b, out, i < nl - 1);
-      if (s) return fail(s, tc_gemm_error());
-      c->launches += tc_gemm_launches(c->tc) - 1;
-      if ((s = launch_check(c, HRP_K_GEMM_FWD))) return s;
+      const float* hi = c->wsplit + (target ? 2 : 0) * c->n_params + c->woff[i];
+      s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h, hi,
+                 hi + c->n_params, b, nullptr, 0, out);
     } else if (i < nl - 1) {
       s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
     } else {
@@ -375,7 +412,14 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     if (i > 0) {
       const float* Wm = c->theta + c->woff[i];
       float* dH = bufs[cur];
-      s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
+      if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(B, fi, fo)) {
+        // dH = dY . W = dY . (W^T)^T with the transposed online split as the B operand
+        const float* hT = c->wsplitT + c->woff[i];
+        s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->n_params,
+                   nullptr, Hin, fi, dH);
+      } else {
+        s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
+      }
       if (s) return s;
       dY = dH;
       cur ^= 1;
@@ -387,9 +431,14 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
 hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.explicit_mode = c->explicit_mode;
   a.n_evals = c->n_evals;
-  const int grid = std::min(a.M, c->sel_grid);
   prof_begin(c);
-  select_kernel<<<grid, kThreads, c->sel_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
+  if (c->explicit_mode) {
+    const int grid = std::min(a.M, c->sel_grid);
+    select_kernel<<<grid, kThreads, c->sel_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
+  } else {
+    const int grid = std::min((a.M + kPWarps - 1) / kPWarps, c->p_grid);
+    pwarp_select_kernel<<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
+  }
   return launch_check(c, HRP_K_SELECT);
 }
 
@@ -605,10 +654,25 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   int occ = 1;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_kernel, kThreads, c->sel_smem));
   c->sel_grid = nsm * std::max(1, occ);
+  c->p_smem = pwarp_smem_bytes(hs.L, hs.T);
+  {
+    static int p_smem_max[64] = {0};
+    if ((int)c->p_smem > p_smem_max[device & 63]) {
+      CK(cudaFuncSetAttribute(pwarp_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem));
+      CK(cudaFuncSetAttribute(pwarp_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem));
+      p_smem_max[device & 63] = (int)c->p_smem;
+    }
+  }
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pwarp_select_kernel, kPWarps * 32, c->p_smem));
+  c->p_grid = nsm * std::max(1, occ);
   if (c->gemm_mode == 2) {
     if ((s = tc_gemm_create(&c->tc, device, (int)R, c->dims.data(), (int)c->dims.size()))) {
       return fail(s, tc_gemm_error());
     }
+    CK(ar.alloc((void**)&c->wsplit, sizeof(float) * 4 * o));
+    CK(ar.alloc((void**)&c->wsplitT, sizeof(float) * 2 * o));
+    if ((s = split_weights(c.get(), false))) return s;
+    if ((s = split_weights(c.get(), true))) return s;
   }
   if (world > 1) {
     ncclUniqueId id;
@@ -747,7 +811,11 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.astar = d_astar;
   t.n_evals = c->n_evals;
   prof_begin(c);
-  td_kernel<<<std::min(B, c->sel_grid), kThreads, c->sel_smem, c->stream>>>(c->dt.sp, t);
+  if (c->explicit_mode)
+    td_kernel<<<std::min(B, c->sel_grid), kThreads, c->sel_smem, c->stream>>>(c->dt.sp, t);
+  else
+    pwarp_td_kernel<<<std::min((B + kPWarps - 1) / kPWarps, c->p_grid), kPWarps * 32, c->p_smem,
+                      c->stream>>>(c->dt.sp, t);
   if ((s = launch_check(c, HRP_K_TD))) return s;
   prof_begin(c);
   loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
@@ -763,6 +831,8 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   sgd_kernel<<<4 * 148, 256, 0, c->stream>>>(c->n_params, c->cfg.lr, c->theta, c->grad, c->theta_t,
                                               sync_target);
   if ((s = launch_check(c, HRP_K_SGD))) return s;
+  if ((s = split_weights(c, false))) return s;
+  if (sync_target && (s = split_weights(c, true))) return s;
   (void)H;
   return HRP_OK;
 }
@@ -864,6 +934,8 @@ hrp_status hrp_set_weights(hrp_ctx* c, const float* in) {
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->theta, in, sizeof(float) * c->n_params, cudaMemcpyHostToDevice, c->stream));
   CK(cudaMemcpyAsync(c->theta_t, in + c->n_params, sizeof(float) * c->n_params, cudaMemcpyHostToDevice, c->stream));
+  hrp_status s;
+  if ((s = split_weights(c, false)) || (s = split_weights(c, true))) return s;
   CK(cudaStreamSynchronize(c->stream));
   return HRP_OK;
 }

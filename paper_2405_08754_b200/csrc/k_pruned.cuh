@@ -1,0 +1,410 @@
+// Warp-per-state kernels for the exact top-C pruned argmax (reading R15):
+//   pwarp_select_kernel  a4-a7 fused (centering, fixed point, greedy argmax, epsilon-greedy,
+//                        co-run reward, transition, replay insert, auto-reset) or inference
+//   pwarp_td_kernel      a9-a10 (double-DQN target argmax on s', target Q, TD error, loss
+//                        term, structured head gradient)
+// One warp owns one state at a time; no block-wide barriers.  The head row z is read from
+// global memory (L2-resident, coalesced across lanes); per warp only the slot-type means and
+// the Top-C lists live in shared memory.
+//
+// Exactness: Top_tau = the C best unscheduled positions by (F(cJ[j][tau]) desc, j asc); any
+// lowest-index maximiser uses only Top-list jobs (exchange argument, oracle/pruned.py).  Per
+// layout the <= C^C assignments are searched depth-first in descending-value order with the
+// bound "partial + sum of the remaining slots' best < best so far => stop" -- valid because
+// the lists are sorted, and ties (== best) are still visited so the lowest index wins.
+#pragma once
+#include "dev.cuh"
+#include "k_env.cuh"
+
+namespace hrp {
+
+constexpr int kPWarps = 8;  // warps (states in flight) per CTA
+
+struct PWarpSmem {
+  float* meanJ;       // [T]
+  int* top;           // [T][4] positions
+  int64_t* topv;      // [T][4] F values
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__host__ __device__ inline size_t pwarp_smem_bytes(int L, int T) {
+  size_t per_warp = align16(sizeof(float) * T) + align16(sizeof(int) * T * 4) +
+                    align16(sizeof(int64_t) * T * 4);
+  size_t tabs = align16(sizeof(int64_t) * (L + 1)) + align16(sizeof(uint32_t) * L) + align16(L);
+  return tabs + kPWarps * per_warp;
+}
+
+struct PTabs {
+  int64_t* off;
+  uint32_t* stype;
+  uint8_t* nsl;
+};
+
+__device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem& w) {
+  PTabs t;
+  size_t o = 0;
+  auto take = [&](size_t b) { uint8_t* p = base + o; o += align16(b); return p; };
+  t.off = (int64_t*)take(sizeof(int64_t) * (sp.L + 1));
+  t.stype = (uint32_t*)take(sizeof(uint32_t) * sp.L);
+  t.nsl = (uint8_t*)take(sp.L);
+  const int wi = threadIdx.x >> 5;
+  const size_t per_warp = align16(sizeof(float) * sp.T) + align16(sizeof(int) * sp.T * 4) +
+                          align16(sizeof(int64_t) * sp.T * 4);
+  uint8_t* wb = base + o + wi * per_warp;
+  w.meanJ = (float*)wb;
+  w.top = (int*)(wb + align16(sizeof(float) * sp.T));
+  w.topv = (int64_t*)(wb + align16(sizeof(float) * sp.T) + align16(sizeof(int) * sp.T * 4));
+  for (int i = threadIdx.x; i <= sp.L; i += blockDim.x) t.off[i] = sp.off[i];
+  for (int i = threadIdx.x; i < sp.L; i += blockDim.x) {
+    t.stype[i] = sp.lay_stype[i];
+    t.nsl[i] = sp.lay_n[i];
+  }
+  __syncthreads();
+  return t;
+}
+
+// Means of a head row (global z): returns meanL, fills meanJ[T] (warp-local smem).
+__device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict__ z, float* meanJ) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();  // previous readers of meanJ are done
+  float a = 0.f;
+  for (int l = lane; l < sp.L; l += 32) a += z[1 + l];
+  const float meanL = warp_sum(a) / (float)sp.L;
+  const float* aJ = z + 1 + sp.L;
+  for (int t = lane; t < sp.T; t += 32) {
+    float s = 0.f;
+    for (int j = 0; j < sp.W; ++j) s += aJ[j * sp.T + t];
+    meanJ[t] = s / (float)sp.W;
+  }
+  __syncwarp();
+  return meanL;
+}
+
+// F(cJ[j][tau]) from global z
+__device__ __forceinline__ int64_t Fj(const DevSpace& sp, const float* z, const float* meanJ, int j,
+                                      int t) {
+  return fixed_point(z[1 + sp.L + j * sp.T + t] - meanJ[t]);
+}
+
+// Greedy (exact pruned) argmax of one state by one warp.  Returns (best, bidx) in all lanes;
+// bidx = INT64_MAX when no action is valid.
+__device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
+                                    const float* __restrict__ z, float meanL, uint64_t sched,
+                                    int64_t& best, int64_t& bidx, int64_t& nevals) {
+  const int lane = threadIdx.x & 31;
+  const int W = sp.W, T = sp.T, cm = sp.cmax;
+  for (int t = lane; t < T; t += 32) {
+    int64_t bv[4] = {INT64_MIN, INT64_MIN, INT64_MIN, INT64_MIN};
+    int bj[4] = {-1, -1, -1, -1};
+    for (int j = 0; j < W; ++j) {
+      if ((sched >> j) & 1ull) continue;
+      const int64_t v = Fj(sp, z, w.meanJ, j, t);
+      if (v <= bv[cm - 1]) continue;  // strictly better than the current last (ties keep lower j)
+      int pos = cm - 1;
+      while (pos > 0 && bv[pos - 1] < v) {
+        bv[pos] = bv[pos - 1];
+        bj[pos] = bj[pos - 1];
+        --pos;
+      }
+      bv[pos] = v;
+      bj[pos] = j;
+    }
+    for (int q = 0; q < 4; ++q) {
+      w.top[t * 4 + q] = bj[q];
+      w.topv[t * 4 + q] = bv[q];
+    }
+  }
+  __syncwarp();
+  const int64_t Fv = fixed_point(z[0]);
+  best = INT64_MIN;
+  bidx = INT64_MAX;
+  for (int l = lane; l < sp.L; l += 32) {
+    const int C = tb.nsl[l];
+    const uint32_t ty = tb.stype[l];
+    int tk[4];
+    bool ok = true;
+    for (int k = 0; k < C; ++k) {
+      tk[k] = (ty >> (8 * k)) & 255;
+      if (w.top[tk[k] * 4 + C - 1] < 0) ok = false;  // fewer than C unscheduled jobs
+    }
+    if (!ok) continue;
+    const int64_t base = Fv + fixed_point(z[1 + l] - meanL);
+    int64_t ub[5];
+    ub[C] = 0;
+    for (int k = C - 1; k >= 0; --k) ub[k] = ub[k + 1] + w.topv[tk[k] * 4];
+    int q[4] = {0, 0, 0, 0};
+    int js[4];
+    int64_t part[5];
+    part[0] = base;
+    int k = 0;
+    // iterative DFS over slot k choosing q[k] in 0..C-1 (values descending)
+    while (k >= 0) {
+      if (q[k] >= C) {  // exhausted this level
+        q[k] = 0;
+        --k;
+        if (k >= 0) ++q[k];
+        continue;
+      }
+      const int j = w.top[tk[k] * 4 + q[k]];
+      const int64_t v = part[k] + w.topv[tk[k] * 4 + q[k]];
+      if (v + ub[k + 1] < best) {  // sorted: later choices at this level are no better
+        q[k] = C;
+        continue;
+      }
+      bool dup = false;
+      for (int i = 0; i < k; ++i) dup |= js[i] == j;
+      if (dup) { ++q[k]; continue; }
+      js[k] = j;
+      if (k == C - 1) {
+        ++nevals;
+        if (v >= best) {
+          int g[4], sg[4];
+          for (int i = 0; i < C; ++i) {
+            int r = 0;
+            for (int i2 = 0; i2 < C; ++i2) r += js[i2] < js[i];
+            g[r] = js[i];
+            sg[r] = i;
+          }
+          const int64_t idx = tb.off[l] + rank_comb(g, C, W) * c_fact[C] + lehmer(sg, C);
+          if (v > best || idx < bidx) { best = v; bidx = idx; }
+        }
+        ++q[k];
+      } else {
+        part[k + 1] = v;
+        ++k;
+        q[k] = 0;
+      }
+    }
+  }
+  warp_best(best, bidx);
+}
+
+// k-th valid action (index order), warp-parallel over layouts.
+__device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, uint64_t sched,
+                                          int64_t k) {
+  const int lane = threadIdx.x & 31;
+  const int W = sp.W;
+  const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
+  const uint64_t freem = all & ~sched;
+  const int U = __popcll(freem);
+  for (int l0 = 0; l0 < sp.L; l0 += 32) {
+    const int l = l0 + lane;
+    int64_t cnt = 0;
+    int C = 0;
+    if (l < sp.L) {
+      C = tb.nsl[l];
+      cnt = 1;
+      for (int i = 0; i < C; ++i) cnt *= (U - i);
+      if (U < C) cnt = 0;
+    }
+    int64_t incl = cnt;  // inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int64_t excl = incl - cnt;
+    const unsigned hit = __ballot_sync(0xffffffffu, l < sp.L && k >= excl && k < incl);
+    if (hit) {
+      const int src = __ffs(hit) - 1;
+      int64_t res = -1;
+      if (lane == src) {
+        const int64_t kk = k - excl;
+        const int64_t f = c_fact[C];
+        const int64_t rg = kk / f, rs = kk - rg * f;
+        int gp[4], g[4];
+        unrank_comb(rg, U, C, gp);
+        for (int i = 0; i < C; ++i) {
+          uint64_t m = freem;
+          for (int x = 0; x < gp[i]; ++x) m &= m - 1;
+          g[i] = __ffsll((long long)m) - 1;
+        }
+        res = tb.off[l] + rank_comb(g, C, W) * f + rs;
+      }
+      return __shfl_sync(0xffffffffu, res, src);
+    }
+    k -= __shfl_sync(0xffffffffu, incl, 31);
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kPWarps * 32)
+pwarp_select_kernel(DevSpace sp, DevPool pool, SelArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  PWarpSmem w;
+  PTabs tb = pload_tabs(sp, smem_raw, w);
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kPWarps + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kPWarps;
+  const int W = sp.W;
+  int64_t nevals = 0;
+  for (int row = gw; row < a.M; row += nw) {
+    const float* z = a.z + (size_t)row * sp.H;
+    const uint64_t sched = a.sched[row];
+    const float meanL = pwarp_means(sp, z, w.meanJ);
+    int64_t best, bidx;
+    pwarp_greedy(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+    if (a.mode == SEL_INFER) {
+      if (lane == 0) {
+        a.actions[row] = bidx == INT64_MAX ? -1 : bidx;
+        a.qmax[row] = bidx == INT64_MAX ? __int_as_float(0x7fc00000)
+                                        : (float)((double)best * (1.0 / 4294967296.0));
+      }
+      __syncwarp();
+      continue;
+    }
+    int64_t act = bidx;
+    if ((uint64_t)a.u_explore[row] < a.thr) {
+      const int64_t nv = n_valid(sp, sched);
+      const int64_t k = (int64_t)__umul64hi(a.u_action[row], (uint64_t)nv);
+      act = pwarp_kth_valid(sp, tb, sched, k);
+    }
+    const uint8_t* wr = a.win + (size_t)row * W;
+    int64_t slot = 0;
+    int d = 0;
+    if (lane == 0) {
+      int g[4], sg[4], jobs[4];
+      const int l = decode_action(sp, act, g, sg);
+      const int C = tb.nsl[l];
+      int64_t solo;
+      const int64_t cr = corun_time(sp, pool, wr, l, g, sg, solo, jobs);
+      double r = ((double)solo / (double)cr - 1.0) * 100.0;
+      if (a.lam != 0.f) {
+        int64_t sc = 0, sm = 0, sT = 0;
+        for (int j = 0; j < W; ++j) { sc += pool.c[wr[j]]; sm += pool.m[wr[j]]; sT += pool.T[wr[j]]; }
+        const double cb = (double)sc / W, mb = (double)sm / W, Tb = (double)sT / W;
+        double ri = 0.0;
+        for (int k = 0; k < C; ++k) {
+          const uint32_t sl = sp.lay_slot[l * 4 + k];
+          const int p = jobs[k];
+          const double dr = (double)pool.T[p] / Tb;
+          ri += ((double)(sl & 0xffff) / 800.0 * ((double)pool.c[p] / cb) +
+                 (double)((sl >> 16) & 255) / 8.0 * ((double)pool.m[p] / mb)) * dr * dr;
+        }
+        r += (double)a.lam * ri;
+      }
+      const float meanLq = meanL;
+      int64_t q = fixed_point(z[0]) + fixed_point(z[1 + l] - meanLq);
+      uint64_t gm = 0;
+      const uint32_t ty = tb.stype[l];
+      for (int i = 0; i < C; ++i) {
+        q += Fj(sp, z, w.meanJ, g[i], (ty >> (8 * sg[i])) & 255);
+        gm |= 1ull << g[i];
+      }
+      const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
+      const uint64_t s2 = sched | gm;
+      d = s2 == all;
+      slot = (a.t_step * (int64_t)a.M + row) % a.N_rep;
+      a.rep_sched[slot] = sched;
+      a.rep_act[slot] = act;
+      a.rep_r[slot] = (float)r;
+      a.rep_done[slot] = (uint8_t)d;
+      a.actions[row] = act;
+      a.rewards[row] = (float)r;
+      a.done[row] = (uint8_t)d;
+      if (a.corun) a.corun[row] = cr;
+      if (a.qsel) a.qsel[row] = (float)((double)q * (1.0 / 4294967296.0));
+      if (a.greedy) a.greedy[row] = bidx;
+      a.sched[row] = d ? 0ull : s2;
+    }
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    d = __shfl_sync(0xffffffffu, d, 0);
+    uint8_t* wm = a.win + (size_t)row * W;
+    for (int j = lane; j < W; j += 32) a.rep_win[slot * W + j] = wm[j];
+    __syncwarp();
+    if (d)
+      for (int j = lane; j < W; j += 32) wm[j] = a.next_win[(size_t)row * W + j];
+    __syncwarp();
+  }
+  if (a.n_evals) {
+    int64_t tot = nevals;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0 && tot) atomicAdd(a.n_evals, (unsigned long long)tot);
+  }
+}
+
+// Float Q(s, a) of action idx from a global head row, warp-cooperative means.
+__device__ inline float pwarp_qfloat(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
+                                     const float* __restrict__ z, int64_t idx, int* l_out,
+                                     int* g_out, int* t_out) {
+  const float meanL = pwarp_means(sp, z, w.meanJ);
+  int g[4], sg[4];
+  const int l = decode_action(sp, idx, g, sg);
+  const uint32_t ty = tb.stype[l];
+  const int C = tb.nsl[l];
+  float q = z[0] + (z[1 + l] - meanL);
+  for (int i = 0; i < C; ++i) {
+    const int t = (ty >> (8 * sg[i])) & 255;
+    q += z[1 + sp.L + g[i] * sp.T + t] - w.meanJ[t];
+    if (g_out) { g_out[i] = g[i]; t_out[i] = t; }
+  }
+  if (l_out) *l_out = l;
+  __syncwarp();
+  return q;
+}
+
+__global__ void __launch_bounds__(kPWarps * 32) pwarp_td_kernel(DevSpace sp, TdArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  PWarpSmem w;
+  PTabs tb = pload_tabs(sp, smem_raw, w);
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kPWarps + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kPWarps;
+  const int H = sp.H, L = sp.L, T = sp.T, W = sp.W;
+  int64_t nevals = 0;
+  for (int b = gw; b < a.B; b += nw) {
+    const bool done = a.bdone[b] != 0;
+    float y = a.br[b];
+    int64_t astar = -1;
+    if (!done) {
+      const float* zn = a.z_all + (size_t)(a.B + b) * H;
+      const float meanL = pwarp_means(sp, zn, w.meanJ);
+      int64_t best;
+      pwarp_greedy(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
+      const float qt = pwarp_qfloat(sp, tb, w, a.z_tgt + (size_t)b * H, astar, nullptr, nullptr,
+                                    nullptr);
+      y = a.br[b] + a.gamma * qt;
+    }
+    int l, g[4], tt[4];
+    const float q = pwarp_qfloat(sp, tb, w, a.z_all + (size_t)b * H, a.bact[b], &l, g, tt);
+    const int C = tb.nsl[l];
+    const float delta = q - y;
+    if (lane == 0) {
+      a.dsq[b] = delta * delta;
+      if (a.astar) a.astar[b] = astar;
+    }
+    const float sc = delta * a.inv_btot;
+    const float invL = 1.f / (float)L, invW = 1.f / (float)W;
+    float* dzr = a.dz + (size_t)b * H;
+    // dQ/dz: v -> 1; aL[l'] -> [l' = l] - 1/L; aJ[j][t] -> #{i: g_i = j, t_i = t} - #{i: t_i = t}/W
+    for (int h = lane; h < H; h += 32) {
+      float dv;
+      if (h == 0) dv = 1.f;
+      else if (h <= L) dv = (h - 1 == l ? 1.f : 0.f) - invL;
+      else {
+        const int qq = h - 1 - L;
+        const int j = qq / T, t = qq - j * T;
+        int cjt = 0, ct = 0;
+        for (int i = 0; i < C; ++i) {
+          ct += tt[i] == t;
+          cjt += (tt[i] == t) && (g[i] == j);
+        }
+        dv = (float)cjt - (float)ct * invW;
+      }
+      dzr[h] = dv * sc;
+    }
+    __syncwarp();
+  }
+  if (a.n_evals) {
+    int64_t tot = nevals;
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0 && tot) atomicAdd(a.n_evals, (unsigned long long)tot);
+  }
+}
+
+}  // namespace hrp
