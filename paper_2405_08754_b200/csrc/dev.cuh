@@ -36,12 +36,15 @@ struct DevPool {
 
 __device__ __forceinline__ uint64_t slot_pack_sm(uint32_t s) { return s & 0xffff; }
 
-static __constant__ int64_t c_binom[65][5];   // binom(n, k), n <= 64, k <= 4 (set by init_constants)
-static __constant__ int64_t c_fact[5];
+// binom(n, k) for n <= 64, k <= 4 and k! (set by init_constants).  Global memory, not
+// __constant__: lanes index them divergently, which the constant cache would serialise.
+static __device__ int64_t c_binom[65][5];
+static __device__ int64_t c_fact[5];
 
 __device__ __forceinline__ int64_t fixed_point(float x) {
-  // F(x) = round-half-even(x * 2^32); exact: fp32 -> fp64 and the power-of-two scale are exact
-  return __double2ll_rn((double)x * 4294967296.0);
+  // F(x) = round-half-even(x * 2^32): the power-of-two scale is exact in fp32 (no overflow for
+  // |x| < 2^95), and cvt.rni.s64.f32 rounds the exact product half-to-even.
+  return __float2ll_rn(x * 4294967296.0f);
 }
 
 // (score desc, idx asc) comparison: true if (s1, i1) is better than (s2, i2).

@@ -1,25 +1,32 @@
-// tcgen05 GEMM for the Q-MLP (SURVEY §8(a) a3 forward, a11 backward-data), sm_100a.
+// tcgen05 GEMM for the Q-MLP (SURVEY §8(a) a3 forward, a11 backward), sm_100a.
 //
 //   D[M][N] = epi( A[M][K] . B[N][K]^T )   fp32 in / fp32 out, 3xTF32 on the tensor cores:
 //   A = A_hi + A_lo, B = B_hi + B_lo (hi = tf32 round-to-nearest, lo = x - hi exactly), and
 //   D ~= A_hi B_hi + A_hi B_lo + A_lo B_hi  (relative error ~2^-21 per product, fp32 accumulate
 //   in TMEM) -- the precision the oracle parity (1e-4, BASELINE north star) needs.
 //
+// Uses (all operands K-major, i.e. row-major with the reduction dimension contiguous):
+//   forward        A = activations [rows][in],  B = W [out][in] (pre-split hi/lo)
+//   backward-data  A = dY [rows][out],          B = W^T [in][out] (pre-split hi/lo)
+//   weight-grad    A = dY^T [out][rows],        B = H^T [in][rows] (split in smem), split-K
+//
 // Structure (one 128 x BN output tile per CTA, 256 threads):
-//   warp 0      TMA producer: A tile (raw fp32, 128 x 32, SWIZZLE_128B) + B_hi/B_lo tiles
-//               (pre-split weights, BN x 32) per stage, mbarrier expect_tx
-//   warp 1      MMA issuer (one elected lane): 3 x tcgen05.mma.kind::tf32 per K=8 step,
+//   warp 0      TMA producer: A tile (raw fp32, 128 x 32, SWIZZLE_128B) + B tiles per stage,
+//               mbarrier expect_tx
+//   warp 1      MMA issuer (one lane): 3 x tcgen05.mma.kind::tf32 per K=8 step,
 //               tcgen05.commit -> stage empty / accumulator full
 //   warp 2      TMEM allocator (BN columns)
-//   warps 4-7   split A in shared memory (hi in place, lo beside it; fence.proxy.async), then
-//               the epilogue: tcgen05.ld 32x32b -> bias / ReLU / ReLU-mask -> global
+//   warps 4-7   split the raw tiles in shared memory (hi in place, lo beside it;
+//               fence.proxy.async), then the epilogue: tcgen05.ld 32x32b -> per-warp 32x33 smem
+//               transpose -> bias / ReLU / ReLU-mask -> coalesced stores of D and (optionally)
+//               of D^T for the first t_rows rows (the backward pass's transposed operands).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
-#include <algorithm>
 #include <string>
 
 #include "gemm_tc.h"
@@ -31,8 +38,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements per K block = 128 bytes = one SWIZZLE_128B row
 constexpr int kThreadsTc = 256;
-
-enum TcEpi { TC_BIAS = 0, TC_BIAS_RELU = 1, TC_RELU_MASK = 2 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -129,12 +134,36 @@ struct TcSmem {
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align*/;
 };
 
-template <int BN, int STAGES, int EPI>
+struct TcArgs {
+  int M, N, K;
+  int boxA, boxB;
+  int kc;                  // K range per blockIdx.z (multiple of BK)
+  const float* bias;
+  const float* aux;        // ReLU mask source [M][ldaux]
+  int ldaux;
+  float* D;                // [M][ldd]; split-K: + blockIdx.z * M * ldd
+  int ldd;
+  float* DT;               // optional D^T [N][ldt] for rows < t_rows
+  int ldt, t_rows;
+};
+
+__device__ __forceinline__ void split_tile(uint8_t* hi, uint8_t* lo, int bytes, int t) {
+  float4* h4 = reinterpret_cast<float4*>(hi);
+  float4* l4 = reinterpret_cast<float4*>(lo);
+  for (int idx = t; idx < bytes / 16; idx += 128) {
+    const float4 x = h4[idx];
+    const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+    h4[idx] = h;
+    l4[idx] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+  }
+}
+
+// SPLITB: B arrives raw through mapB0 and is split in shared memory like A; otherwise mapB0 /
+// mapB1 carry the pre-split hi / lo planes.
+template <int BN, int STAGES, int EPI, bool SPLITB>
 __global__ void __launch_bounds__(kThreadsTc, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapBh,
-               const __grid_constant__ CUtensorMap mapBl, int M, int N, int K, int boxA,
-               int boxB, const float* __restrict__ bias, const float* __restrict__ aux, int ldaux,
-               float* __restrict__ D, int ldd) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
+               const __grid_constant__ CUtensorMap mapB1, const TcArgs a) {
   using S = TcSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -144,19 +173,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   auto b_lo = [&](int s) { return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES + S::B_BYTES; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
   uint64_t* full_bar = bars;               // TMA landed
-  uint64_t* conv_bar = bars + STAGES;      // A split done
+  uint64_t* conv_bar = bars + STAGES;      // split done
   uint64_t* empty_bar = bars + 2 * STAGES; // MMA finished reading the stage
   uint64_t* acc_bar = bars + 3 * STAGES;   // accumulator complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nk = (K + BK - 1) / BK;
+  const int kbeg = blockIdx.z * a.kc;
+  const int kend = min(a.K, kbeg + a.kc);
+  const int nk = (kend - kbeg + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBh)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBl)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB0)) : "memory");
+    if (!SPLITB)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB1)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&conv_bar[s], 128);
@@ -178,13 +210,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 
   if (warp == 0) {
     if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(a.boxA + (SPLITB ? 1 : 2) * a.boxB) * BK * 4;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty_bar[s], ((kb / STAGES) - 1) & 1);
-        mbar_expect_tx(&full_bar[s], (uint32_t)(boxA + 2 * boxB) * BK * 4);
-        tma_load_2d(a_hi(s), &mapA, &full_bar[s], kb * BK, m0);
-        tma_load_2d(b_hi(s), &mapBh, &full_bar[s], kb * BK, n0);
-        tma_load_2d(b_lo(s), &mapBl, &full_bar[s], kb * BK, n0);
+        mbar_expect_tx(&full_bar[s], bytes);
+        const int kk = kbeg + kb * BK;
+        tma_load_2d(a_hi(s), &mapA, &full_bar[s], kk, m0);
+        tma_load_2d(b_hi(s), &mapB0, &full_bar[s], kk, n0);
+        if (!SPLITB) tma_load_2d(b_lo(s), &mapB1, &full_bar[s], kk, n0);
       }
     }
   } else if (warp == 1) {
@@ -210,52 +244,54 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
     }
   } else if (warp >= 4) {
     const int t = threadIdx.x - 128;  // 0..127
-    // ---- split A tiles: hi = rna_tf32(x) in place, lo = x - hi ----
+    // ---- split raw tiles: hi = rna_tf32(x) in place, lo = x - hi ----
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
       mbar_wait(&full_bar[s], (kb / STAGES) & 1);
-      float4* ah = reinterpret_cast<float4*>(a_hi(s));
-      float4* al = reinterpret_cast<float4*>(a_lo(s));
-#pragma unroll
-      for (int i = 0; i < S::A_BYTES / 16 / 128; ++i) {
-        const int idx = i * 128 + t;
-        float4 x = ah[idx];
-        float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-        float4 l = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
-        ah[idx] = h;
-        al[idx] = l;
-      }
+      split_tile(a_hi(s), a_lo(s), S::A_BYTES, t);
+      if (SPLITB) split_tile(b_hi(s), b_lo(s), S::B_BYTES, t);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&conv_bar[s]);
     }
-    // ---- epilogue: TMEM -> registers -> smem (per-warp 32 x 33 transpose) -> coalesced ----
+    // ---- epilogue: TMEM -> registers -> smem (per-warp 32 x 33) -> coalesced D (and D^T) ----
     mbar_wait(acc_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int wq = warp & 3;                 // TMEM lane quarter of this warp = its 32 rows
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     float* stg = reinterpret_cast<float*>(smem) + wq * (32 * 33);  // stage buffers are idle now
     const int rbase = m0 + wq * 32;
+    float* Dz = a.D + (size_t)blockIdx.z * a.M * a.ldd;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t v[32];
       TMEM_LD32(trow + c, v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (n0 + c >= N) break;                // warp-uniform
+      if (n0 + c >= a.N) break;                // warp-uniform
 #pragma unroll
       for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(v[j]);
       __syncwarp();
       const int col = n0 + c + lane;
       float bcol = 0.f;
-      if ((EPI == TC_BIAS || EPI == TC_BIAS_RELU) && col < N) bcol = bias[col];
+      if ((EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) && col < a.N) bcol = a.bias[col];
 #pragma unroll 4
       for (int r = 0; r < 32; ++r) {
         const int row = rbase + r;
-        if (row < M && col < N) {
+        if (row < a.M && col < a.N) {
           float x = stg[r * 33 + lane];
-          if (EPI == TC_BIAS || EPI == TC_BIAS_RELU) x += bcol;
-          if (EPI == TC_BIAS_RELU) x = fmaxf(x, 0.f);
-          if (EPI == TC_RELU_MASK) x = aux[(size_t)row * ldaux + col] > 0.f ? x : 0.f;
-          D[(size_t)row * ldd + col] = x;
+          if (EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) x += bcol;
+          if (EPI == TC_EPI_BIAS_RELU) x = fmaxf(x, 0.f);
+          if (EPI == TC_EPI_RELU_MASK) x = a.aux[(size_t)row * a.ldaux + col] > 0.f ? x : 0.f;
+          Dz[(size_t)row * a.ldd + col] = x;
+          stg[r * 33 + lane] = x;
+        }
+      }
+      __syncwarp();
+      if (a.DT != nullptr && rbase < a.t_rows) {
+        const int row = rbase + lane;
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const int cc = n0 + c + r;
+          if (cc < a.N && row < a.t_rows && row < a.M) a.DT[(size_t)cc * a.ldt + row] = stg[lane * 33 + r];
         }
       }
       __syncwarp();
@@ -300,6 +336,55 @@ __global__ void split_t_kernel(int rows, int cols, const float* __restrict__ w,
   }
 }
 
+// dst[c][r] = src[r][c]
+__global__ void transpose_kernel(int rows, int cols, int ld_src, const float* __restrict__ src,
+                                 int ld_dst, float* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)r * ld_src + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dst[(size_t)c * ld_dst + r] = tile[threadIdx.x][i];
+  }
+}
+
+// out[r] = sum_c src[r][c], one warp per row, fixed (deterministic) order.
+__global__ void rowsum_kernel(int rows, int cols, const float* __restrict__ src,
+                              float* __restrict__ out) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const float* p = src + (size_t)w * cols;
+  float s = 0.f;
+  if ((cols & 3) == 0) {
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    for (int c = lane; c < cols / 4; c += 32) {
+      const float4 v = p4[c];
+      s += (v.x + v.y) + (v.z + v.w);
+    }
+  } else {
+    for (int c = lane; c < cols; c += 32) s += p[c];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s;
+}
+
+// out[i] = sum_z ws[z][i], deterministic
+__global__ void reduce_splits_kernel(int S, int64_t n, const float* __restrict__ ws,
+                                     float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < S; ++z) s += ws[(size_t)z * n + i];
+    out[i] = s;
+  }
+}
+
 thread_local std::string g_tc_err;
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
@@ -326,32 +411,34 @@ bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int box_rows) 
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    g_tc_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    g_tc_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") rows " +
+               std::to_string(rows) + " cols " + std::to_string(cols) + " box " +
+               std::to_string(box_rows);
     return false;
   }
   return true;
 }
 
-template <int BN, int STAGES, int EPI>
-hrp_status launch(cudaStream_t st, int M, int N, int K, const float* A, const float* Bh,
-                  const float* Bl, const float* bias, const float* aux, int ldaux, float* D) {
-  CUtensorMap ma, mbh, mbl;
+template <int BN, int STAGES, int EPI, bool SPLITB>
+hrp_status launch(cudaStream_t st, const float* A, const float* B0, const float* B1, TcArgs a,
+                  int splits) {
+  CUtensorMap ma, mb0, mb1;
   // boxes never exceed the tensor; rows of a tile beyond the box only feed masked outputs
-  const int boxA = std::min(BM, M), boxB = std::min(BN, N);
-  if (!make_map(&ma, A, M, K, boxA) || !make_map(&mbh, Bh, N, K, boxB) ||
-      !make_map(&mbl, Bl, N, K, boxB))
-    return HRP_ECUDA;
+  a.boxA = std::min(BM, a.M);
+  a.boxB = std::min(BN, a.N);
+  if (!make_map(&ma, A, a.M, a.K, a.boxA) || !make_map(&mb0, B0, a.N, a.K, a.boxB)) return HRP_ECUDA;
+  if (!SPLITB && !make_map(&mb1, B1, a.N, a.K, a.boxB)) return HRP_ECUDA;
+  if (SPLITB) mb1 = mb0;
   constexpr int smem = TcSmem<BN, STAGES>::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI, SPLITB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
     attr = true;
   }
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
-  tc_gemm_kernel<BN, STAGES, EPI><<<grid, kThreadsTc, smem, st>>>(ma, mbh, mbl, M, N, K, boxA, boxB,
-                                                                  bias, aux, ldaux, D, N);
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, splits);
+  tc_gemm_kernel<BN, STAGES, EPI, SPLITB><<<grid, kThreadsTc, smem, st>>>(ma, mb0, mb1, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
@@ -361,48 +448,95 @@ hrp_status launch(cudaStream_t st, int M, int N, int K, const float* A, const fl
 
 struct TcGemm {
   int launches = 0;
+  int nsm = 148;
 };
 
-hrp_status tc_gemm_create(TcGemm** out, int, int, const int*, int) {
+hrp_status tc_gemm_create(TcGemm** out, int device, int, const int*, int) {
   if (!get_encode()) return HRP_ECUDA;
   *out = new TcGemm();
+  cudaDeviceGetAttribute(&(*out)->nsm, cudaDevAttrMultiProcessorCount, device);
   return HRP_OK;
 }
 void tc_gemm_destroy(TcGemm* g) { delete g; }
 
 bool tc_gemm_supported(int M, int N, int K) { return M >= 1 && N >= 1 && K >= 4 && K % 4 == 0; }
 
-static int pick_bn(int M, int N) {
-  // wide tiles when there are enough of them to fill 148 SMs, else 128-wide
+static int pick_bn(int M, int N, int nsm) {
+  // wide tiles when there are enough of them to fill the SMs, else 128-wide
   const long t256 = (long)((M + BM - 1) / BM) * ((N + 255) / 256);
-  return (N > 128 && t256 >= 148) ? 256 : 128;
+  return (N > 128 && t256 >= nsm) ? 256 : 128;
 }
 
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, const float* A,
                        const float* Bh, const float* Bl, const float* bias, const float* aux,
-                       int ldaux, float* D) {
+                       int ldaux, float* D, float* DT, int t_rows) {
   g->launches++;
-  const int bn = pick_bn(M, N);
-  if (bn == 256) {
-    if (epi == TC_BIAS) return launch<256, 2, TC_BIAS>(st, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
-    if (epi == TC_BIAS_RELU) return launch<256, 2, TC_BIAS_RELU>(st, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
-    return launch<256, 2, TC_RELU_MASK>(st, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
+  TcArgs a{};
+  a.M = M; a.N = N; a.K = K; a.kc = K;
+  a.bias = bias; a.aux = aux; a.ldaux = ldaux;
+  a.D = D; a.ldd = N;
+  a.DT = DT; a.ldt = t_rows; a.t_rows = DT ? t_rows : 0;
+  if (pick_bn(M, N, g->nsm) == 256) {
+    if (epi == TC_EPI_BIAS) return launch<256, 2, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
+    if (epi == TC_EPI_BIAS_RELU) return launch<256, 2, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
+    return launch<256, 2, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
   }
-  if (epi == TC_BIAS) return launch<128, 3, TC_BIAS>(st, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
-  if (epi == TC_BIAS_RELU) return launch<128, 3, TC_BIAS_RELU>(st, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
-  return launch<128, 3, TC_RELU_MASK>(st, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
+  if (epi == TC_EPI_BIAS) return launch<128, 3, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
+  if (epi == TC_EPI_BIAS_RELU) return launch<128, 3, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
+  return launch<128, 3, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
+}
+
+hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, const float* A,
+                         const float* B, float* ws, size_t ws_elems, float* D) {
+  // D[M][N] = A[M][K] . B[N][K]^T, both raw (split in smem), split-K + deterministic reduce
+  const long tiles = (long)((M + BM - 1) / BM) * ((N + 127) / 128);
+  int S = (int)std::max(1L, std::min(32L, (2L * g->nsm + tiles - 1) / tiles));
+  int kc = (K + S - 1) / S;
+  kc = (kc + BK - 1) / BK * BK;
+  S = (K + kc - 1) / kc;
+  if ((size_t)S * M * N > ws_elems) { g_tc_err = "split-K workspace too small"; return HRP_ENOMEM; }
+  TcArgs a{};
+  a.M = M; a.N = N; a.K = K; a.kc = kc;
+  a.D = S > 1 ? ws : D; a.ldd = N;
+  g->launches++;
+  hrp_status s = launch<128, 3, TC_EPI_STORE, true>(st, A, B, nullptr, a, S);
+  if (s || S == 1) return s;
+  const int64_t n = (int64_t)M * N;
+  reduce_splits_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(S, n, ws, D);
+  g->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
+  return HRP_OK;
 }
 
 hrp_status tc_split(TcGemm* g, cudaStream_t st, int rows, int cols, const float* w, float* hi,
                     float* lo, float* hiT, float* loT) {
   const int64_t n = (int64_t)rows * cols;
-  split_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, st>>>(n, w, hi, lo);
+  split_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(n, w, hi, lo);
   g->launches++;
   if (hiT) {
     dim3 grid((cols + 31) / 32, (rows + 31) / 32);
     split_t_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, w, hiT, loT);
     g->launches++;
   }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
+  return HRP_OK;
+}
+
+hrp_status tc_transpose(TcGemm* g, cudaStream_t st, int rows, int cols, int ld_src,
+                        const float* src, int ld_dst, float* dst) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, ld_src, src, ld_dst, dst);
+  g->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
+  return HRP_OK;
+}
+
+hrp_status tc_rowsum(TcGemm* g, cudaStream_t st, int rows, int cols, const float* src, float* out) {
+  rowsum_kernel<<<(rows + 7) / 8, 256, 0, st>>>(rows, cols, src, out);
+  g->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;

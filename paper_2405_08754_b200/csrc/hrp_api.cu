@@ -214,6 +214,8 @@ struct hrp_ctx {
   // 3xTF32 operand splits for the tcgen05 GEMMs: [online hi | online lo | target hi | target lo]
   // in the flat parameter layout, and the online weights transposed ([in][out]) hi | lo.
   float *wsplit = nullptr, *wsplitT = nullptr;
+  std::vector<int64_t> soff;  // per-layer weight offsets in a split plane (128-B aligned for TMA)
+  int64_t sstride = 0;        // floats per split plane
   size_t ws_splitk_elems = 0;
   // env state
   uint8_t* win = nullptr;
@@ -233,6 +235,10 @@ struct hrp_ctx {
   float* zt = nullptr;                // [B][H]
   float* dz = nullptr;                // [B][H]
   float *dh0 = nullptr, *dh1 = nullptr;  // [B][w]
+  // transposed operands of the tensor-core backward: X^T [in][B], hidden outputs^T [w][B],
+  // dz^T [H][B], dh^T [w][B]
+  float *XT = nullptr, *dzT = nullptr, *dhT0 = nullptr, *dhT1 = nullptr;
+  std::vector<float*> actT;
   uint8_t* bwin = nullptr;            // [2B][W] or [chunk][W]
   uint64_t* bsched = nullptr;
   int64_t* bact = nullptr;
@@ -335,15 +341,15 @@ hrp_status split_weights(hrp_ctx* c, bool target) {
   if (!c->tc) return HRP_OK;
   const int nl = (int)c->dims.size() - 1;
   const float* th = target ? c->theta_t : c->theta;
-  float* hi = c->wsplit + (target ? 2 : 0) * c->n_params;
-  float* lo = hi + c->n_params;
+  float* hi = c->wsplit + (target ? 2 : 0) * c->sstride;
+  float* lo = hi + c->sstride;
   for (int i = 0; i < nl; ++i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
-    const int64_t o = c->woff[i];
-    float* hT = target ? nullptr : c->wsplitT + o;
-    float* lT = target ? nullptr : c->wsplitT + c->n_params + o;
+    const int64_t o = c->woff[i], so = c->soff[i];
+    float* hT = target ? nullptr : c->wsplitT + so;
+    float* lT = target ? nullptr : c->wsplitT + c->sstride + so;
     prof_begin(c);
-    hrp_status s = tc_split(c->tc, c->stream, fo, fi, th + o, hi + o, lo + o, hT, lT);
+    hrp_status s = tc_split(c->tc, c->stream, fo, fi, th + o, hi + so, lo + so, hT, lT);
     if (s) return fail(s, tc_gemm_error());
     c->launches += tc_gemm_launches(c->tc) - 1;
     if ((s = launch_check(c, HRP_K_SGD))) return s;
@@ -351,20 +357,37 @@ hrp_status split_weights(hrp_ctx* c, bool target) {
   return HRP_OK;
 }
 
-// Tensor-core GEMM D = epi(A . B^T) with pre-split B (hi, lo).
+// Tensor-core GEMM D = epi(A . B^T) with pre-split B (hi, lo); optional transposed copy DT of
+// the first t_rows rows of D.
 hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, const float* A,
                   const float* Bh, const float* Bl, const float* bias, const float* aux, int ldaux,
-                  float* D) {
+                  float* D, float* DT = nullptr, int t_rows = 0) {
   prof_begin(c);
-  hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, Bh, Bl, bias, aux, ldaux, D);
+  hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, Bh, Bl, bias, aux, ldaux, D, DT,
+                             t_rows);
   if (s) return fail(s, tc_gemm_error());
   c->launches += tc_gemm_launches(c->tc) - 1;
   return launch_check(c, cls);
 }
 
+// Transposed copy dst [cols][rows] of src [rows][cols] (ld_src) on the tensor-core path.
+hrp_status transpose(hrp_ctx* c, int cls, int rows, int cols, int ld_src, const float* src,
+                     float* dst) {
+  prof_begin(c);
+  hrp_status s = tc_transpose(c->tc, c->stream, rows, cols, ld_src, src, rows, dst);
+  if (s) return fail(s, tc_gemm_error());
+  c->launches += tc_gemm_launches(c->tc) - 1;
+  return launch_check(c, cls);
+}
+
+// The tensor-core backward needs B % 4 == 0 (TMA row stride of the transposed operands).
+bool tc_backward(const hrp_ctx* c, int B) { return c->gemm_mode == 2 && c->tc && B % 4 == 0; }
+
 // Forward of one network over M rows of X: hidden outputs to c->act (kept for the backward
-// pass), head output z_out [M][H].
-hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out) {
+// pass), head output z_out [M][H].  With t_rows > 0 the first t_rows rows of every hidden
+// output are also stored transposed in c->actT (operands of the weight-gradient GEMMs).
+hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out,
+                       int t_rows = 0) {
   c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
   const bool target = theta == c->theta_t;
@@ -374,15 +397,18 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, fl
     const float* Wm = theta + c->woff[i];
     const float* b = Wm + (int64_t)fi * fo;
     float* out = (i == nl - 1) ? z_out : c->act[i];
+    float* outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : nullptr;
     hrp_status s;
     if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(M, fo, fi)) {
-      const float* hi = c->wsplit + (target ? 2 : 0) * c->n_params + c->woff[i];
+      const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
       s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h, hi,
-                 hi + c->n_params, b, nullptr, 0, out);
-    } else if (i < nl - 1) {
-      s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
+                 hi + c->sstride, b, nullptr, 0, out, outT, t_rows);
     } else {
-      s = sgemm<true, true, EPI_BIAS>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
+      if (i < nl - 1)
+        s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
+      else
+        s = sgemm<true, true, EPI_BIAS>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
+      if (!s && outT) s = transpose(c, HRP_K_GEMM_FWD, t_rows, fo, fo, out, outT);
     }
     if (s) return s;
     h = out;
@@ -390,8 +416,60 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, fl
   return HRP_OK;
 }
 
+// Backward over the first B rows on the tensor cores: operands are the transposed copies
+// (XT, actT, dzT) so every GEMM is K-major.  dz [B][H] -> c->grad.
+hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
+  c->gemm_cls = HRP_K_GEMM_BWD;
+  const int nl = (int)c->dims.size() - 1;
+  const int H = c->dims[nl];
+  hrp_status s;
+  if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, H, c->dz, c->dzT))) return s;
+  const float* dY = c->dz;
+  const float* dYT = c->dzT;
+  float* bufs[2] = {c->dh0, c->dh1};
+  float* bufsT[2] = {c->dhT0, c->dhT1};
+  int cur = 0;
+  for (int i = nl - 1; i >= 0; --i) {
+    const int fi = c->dims[i], fo = c->dims[i + 1];
+    const float* HinT = (i == 0) ? c->XT : c->actT[i - 1];
+    const float* Hin = (i == 0) ? c->X : c->act[i - 1];
+    float* gW = c->grad + c->woff[i];
+    float* gb = gW + (int64_t)fi * fo;
+    // dW [fo][fi] = dY^T . Hin = (dYT [fo][B]) . (HinT [fi][B])^T
+    prof_begin(c);
+    s = tc_gemm_wgrad(c->tc, c->stream, fo, fi, B, dYT, HinT, c->ws_splitk, c->ws_splitk_elems, gW);
+    if (s) return fail(s, tc_gemm_error());
+    c->launches += tc_gemm_launches(c->tc) - 1;
+    if ((s = launch_check(c, HRP_K_GEMM_BWD))) return s;
+    prof_begin(c);
+    s = tc_rowsum(c->tc, c->stream, fo, B, dYT, gb);
+    if (s) return fail(s, tc_gemm_error());
+    c->launches += tc_gemm_launches(c->tc) - 1;
+    if ((s = launch_check(c, HRP_K_GEMM_BWD))) return s;
+    if (i > 0) {
+      float* dH = bufs[cur];
+      float* dHT = bufsT[cur];
+      if (tc_gemm_supported(B, fi, fo)) {
+        const float* hT = c->wsplitT + c->soff[i];
+        s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->sstride,
+                   nullptr, Hin, fi, dH, dHT, B);
+      } else {
+        const float* Wm = c->theta + c->woff[i];
+        s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
+        if (!s) s = transpose(c, HRP_K_GEMM_BWD, B, fi, fi, dH, dHT);
+      }
+      if (s) return s;
+      dY = dH;
+      dYT = dHT;
+      cur ^= 1;
+    }
+  }
+  return HRP_OK;
+}
+
 // Backward over the first B rows (X rows [0,B), act rows [0,B)), dz [B][H] -> c->grad.
 hrp_status mlp_backward(hrp_ctx* c, int B) {
+  if (tc_backward(c, B)) return mlp_backward_tc(c, B);
   c->gemm_cls = HRP_K_GEMM_BWD;
   const int nl = (int)c->dims.size() - 1;
   const float* dY = c->dz;
@@ -414,8 +492,8 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
       float* dH = bufs[cur];
       if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(B, fi, fo)) {
         // dH = dY . W = dY . (W^T)^T with the transposed online split as the B operand
-        const float* hT = c->wsplitT + c->woff[i];
-        s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->n_params,
+        const float* hT = c->wsplitT + c->soff[i];
+        s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->sstride,
                    nullptr, Hin, fi, dH);
       } else {
         s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
@@ -588,6 +666,14 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     o += (int64_t)c->dims[i] * c->dims[i + 1] + c->dims[i + 1];
   }
   c->n_params = o;
+  {
+    int64_t so = 0;
+    for (size_t i = 0; i + 1 < c->dims.size(); ++i) {
+      c->soff.push_back(so);
+      so += ((int64_t)c->dims[i] * c->dims[i + 1] + 31) / 32 * 32;
+    }
+    c->sstride = so;
+  }
   const int E = cfg->n_envs, B = cfg->batch, W = hs.W, H = hs.head_width();
   const int in = c->dims[0], wd = cfg->hidden_width;
   c->rows_max = std::max({E, 2 * B, 8192});
@@ -622,6 +708,15 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->dz, sizeof(float) * (size_t)B * H));
   CK(ar.alloc((void**)&c->dh0, sizeof(float) * (size_t)B * wd));
   CK(ar.alloc((void**)&c->dh1, sizeof(float) * (size_t)B * wd));
+  CK(ar.alloc((void**)&c->XT, sizeof(float) * (size_t)B * in));
+  CK(ar.alloc((void**)&c->dzT, sizeof(float) * (size_t)B * H));
+  CK(ar.alloc((void**)&c->dhT0, sizeof(float) * (size_t)B * wd));
+  CK(ar.alloc((void**)&c->dhT1, sizeof(float) * (size_t)B * wd));
+  for (int i = 0; i < cfg->hidden_layers; ++i) {
+    float* p;
+    CK(ar.alloc((void**)&p, sizeof(float) * (size_t)B * wd));
+    c->actT.push_back(p);
+  }
   CK(ar.alloc((void**)&c->bwin, R * W));
   CK(ar.alloc((void**)&c->bsched, R * 8));
   CK(ar.alloc((void**)&c->bact, R * 8));
@@ -669,8 +764,8 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     if ((s = tc_gemm_create(&c->tc, device, (int)R, c->dims.data(), (int)c->dims.size()))) {
       return fail(s, tc_gemm_error());
     }
-    CK(ar.alloc((void**)&c->wsplit, sizeof(float) * 4 * o));
-    CK(ar.alloc((void**)&c->wsplitT, sizeof(float) * 2 * o));
+    CK(ar.alloc((void**)&c->wsplit, sizeof(float) * 4 * c->sstride));
+    CK(ar.alloc((void**)&c->wsplitT, sizeof(float) * 2 * c->sstride));
     if ((s = split_weights(c.get(), false))) return s;
     if ((s = split_weights(c.get(), true))) return s;
   }
@@ -783,8 +878,10 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   encode_kernel<<<(2 * B + 7) / 8, 256, 0, c->stream>>>(2 * B, c->hs.W, c->bwin, c->bsched,
                                                          c->dt.pool, c->X);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
+  const bool tcb = tc_backward(c, B);
+  if (tcb && (s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->dims[0], c->X, c->XT))) return s;
   // online net on [s; s'] (activations of the s rows kept for backward), target on s'
-  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z))) return s;
+  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, tcb ? B : 0))) return s;
   // target forward reuses act buffers rows [B,2B) scratch: run on X rows [B,2B) into zt
   {
     // hidden activations of the target pass must not clobber rows [0,B) kept for backward:

@@ -83,7 +83,9 @@ def test_explicit_equals_pruned_full_size():
     a1, q1, _ = s1.q_forward(dw, ds)
     a2, q2, _ = s2.q_forward(dw, ds)
     torch.cuda.synchronize()
-    assert torch.equal(a1, a2) and torch.equal(q1, q2)
+    # argmax bit-exact; Q^max agrees to fp32 rounding of the (differently ordered) mean sums
+    assert torch.equal(a1, a2)
+    assert torch.allclose(q1, q2, rtol=1e-6, atol=1e-6)
 
 
 def test_config4_pruned_q_forward_sampled():
