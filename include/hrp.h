@@ -203,6 +203,13 @@ hrp_status hrp_profile_read(hrp_ctx *ctx, double *ms, int64_t *launches);
 /* Explicit Q^ evaluations (valid (l, g, sigma) scored; pruned mode: candidate assignments)
  * counted by the selection kernels since create (synchronises the stream). */
 int64_t hrp_eval_count(hrp_ctx *ctx);
+/* Diagnostics: one tensor-core GEMM D[M][N] = A[M][K] . W[N][K]^T + bias (3xTF32, the Q-MLP
+ * forward kernel) on `device` / `cuda_stream`, all pointers device; d_trace (optional,
+ * uint64 [256]) receives %globaltimer stamps of CTA (0,0): [0] start, [1] setup, [2+kb] TMA
+ * issue, [66+kb] split done, [130+kb] MMA issued, [194] accumulator ready, [195] end. */
+hrp_status hrp_diag_gemm(int device, void *cuda_stream, int M, int N, int K, const float *d_A,
+                         const float *d_W, const float *d_bias, float *d_D,
+                         uint64_t *d_trace);
 /* Block until the context's stream is idle; returns any pending CUDA/NCCL error. */
 hrp_status hrp_sync(hrp_ctx *ctx);
 const char *hrp_last_error(void);

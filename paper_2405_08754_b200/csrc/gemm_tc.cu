@@ -145,7 +145,20 @@ struct TcArgs {
   int ldd;
   float* DT;               // optional D^T [N][ldt] for rows < t_rows
   int ldt, t_rows;
+  unsigned long long* trace;  // diagnostics: per-event timestamps of CTA (0,0,0), or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// trace slots: [0] start, [1] setup done, [2+kb] TMA issued, [66+kb] split done,
+// [130+kb] MMA issued, [194] acc ready, [195] epilogue done
+#define TRACE(slot)                                                                         \
+  do {                                                                                      \
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) a.trace[slot] = gtimer(); \
+  } while (0)
 
 __device__ __forceinline__ void split_tile(uint8_t* hi, uint8_t* lo, int bytes, int t) {
   float4* h4 = reinterpret_cast<float4*>(hi);
@@ -183,6 +196,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   const int kbeg = blockIdx.z * a.kc;
   const int kend = min(a.K, kbeg + a.kc);
   const int nk = (kend - kbeg + BK - 1) / BK;
+  if (threadIdx.x == 0) TRACE(0);
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
@@ -207,6 +221,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -219,6 +234,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
         tma_load_2d(a_hi(s), &mapA, &full_bar[s], kk, m0);
         tma_load_2d(b_hi(s), &mapB0, &full_bar[s], kk, n0);
         if (!SPLITB) tma_load_2d(b_lo(s), &mapB1, &full_bar[s], kk, n0);
+        if (kb < 64) TRACE(2 + kb);
       }
     }
   } else if (warp == 1) {
@@ -239,11 +255,19 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
           mma_tf32(tmem, dal + adv, dbh + adv, idesc, 1u);
         }
         mma_commit(&empty_bar[s]);
+        if (kb < 64) TRACE(130 + kb);
       }
       mma_commit(acc_bar);
     }
   } else if (warp >= 4) {
     const int t = threadIdx.x - 128;  // 0..127
+    if (EPI == TC_EPI_RELU_MASK) {
+      // warm L2 with this tile's ReLU-mask rows now, so the epilogue's reads do not stall
+      const int row = m0 + t;
+      if (row < a.M)
+        for (int cb = n0; cb < min(a.N, n0 + BN); cb += 32)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.aux + (size_t)row * a.ldaux + cb));
+    }
     // ---- split raw tiles: hi = rna_tf32(x) in place, lo = x - hi ----
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % STAGES;
@@ -252,35 +276,51 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
       if (SPLITB) split_tile(b_hi(s), b_lo(s), S::B_BYTES, t);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&conv_bar[s]);
+      if (t == 0 && kb < 64) TRACE(66 + kb);
     }
     // ---- epilogue: TMEM -> registers -> smem (per-warp 32 x 33) -> coalesced D (and D^T) ----
+    const int wq = warp & 3;                 // TMEM lane quarter of this warp = its 32 rows
+    const int rbase = m0 + wq * 32;
+    // bias of every column chunk this lane will write, loaded before the accumulator is ready
+    float bias_r[BN / 32];
+#pragma unroll
+    for (int q = 0; q < BN / 32; ++q) {
+      const int col = n0 + q * 32 + lane;
+      bias_r[q] = ((EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) && col < a.N) ? a.bias[col] : 0.f;
+    }
     mbar_wait(acc_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const int wq = warp & 3;                 // TMEM lane quarter of this warp = its 32 rows
+    if (t == 0) TRACE(194);
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     float* stg = reinterpret_cast<float*>(smem) + wq * (32 * 33);  // stage buffers are idle now
-    const int rbase = m0 + wq * 32;
     float* Dz = a.D + (size_t)blockIdx.z * a.M * a.ldd;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+#pragma unroll
+    for (int q = 0; q < BN / 32; ++q) {
+      const int c = q * 32;
       uint32_t v[32];
       TMEM_LD32(trow + c, v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (n0 + c >= a.N) break;                // warp-uniform
+      const int col = n0 + c + lane;
+      float mk[32];
+      if (EPI == TC_EPI_RELU_MASK) {           // all 32 mask loads in flight at once
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+          const int row = rbase + r;
+          mk[r] = (row < a.M && col < a.N) ? a.aux[(size_t)row * a.ldaux + col] : 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(v[j]);
       __syncwarp();
-      const int col = n0 + c + lane;
-      float bcol = 0.f;
-      if ((EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) && col < a.N) bcol = a.bias[col];
-#pragma unroll 4
+#pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int row = rbase + r;
         if (row < a.M && col < a.N) {
           float x = stg[r * 33 + lane];
-          if (EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) x += bcol;
+          if (EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) x += bias_r[q];
           if (EPI == TC_EPI_BIAS_RELU) x = fmaxf(x, 0.f);
-          if (EPI == TC_EPI_RELU_MASK) x = a.aux[(size_t)row * a.ldaux + col] > 0.f ? x : 0.f;
+          if (EPI == TC_EPI_RELU_MASK) x = mk[r] > 0.f ? x : 0.f;
           Dz[(size_t)row * a.ldd + col] = x;
           stg[r * 33 + lane] = x;
         }
@@ -299,6 +339,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (threadIdx.x == 0) TRACE(195);
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
   }
@@ -462,24 +503,33 @@ void tc_gemm_destroy(TcGemm* g) { delete g; }
 bool tc_gemm_supported(int M, int N, int K) { return M >= 1 && N >= 1 && K >= 4 && K % 4 == 0; }
 
 static int pick_bn(int M, int N, int nsm) {
-  // wide tiles when there are enough of them to fill the SMs, else 128-wide
-  const long t256 = (long)((M + BM - 1) / BM) * ((N + 255) / 256);
-  return (N > 128 && t256 >= nsm) ? 256 : 128;
+  // the widest tile that still gives every SM a tile; narrow tiles for small problems
+  const long mt = (M + BM - 1) / BM;
+  if (N > 128 && mt * ((N + 255) / 256) >= nsm) return 256;
+  if (N > 64 && mt * ((N + 127) / 128) >= nsm) return 128;
+  return 64;
 }
 
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, const float* A,
                        const float* Bh, const float* Bl, const float* bias, const float* aux,
-                       int ldaux, float* D, float* DT, int t_rows) {
+                       int ldaux, float* D, float* DT, int t_rows, unsigned long long* trace) {
   g->launches++;
   TcArgs a{};
+  a.trace = trace;
   a.M = M; a.N = N; a.K = K; a.kc = K;
   a.bias = bias; a.aux = aux; a.ldaux = ldaux;
   a.D = D; a.ldd = N;
   a.DT = DT; a.ldt = t_rows; a.t_rows = DT ? t_rows : 0;
-  if (pick_bn(M, N, g->nsm) == 256) {
+  const int bn = pick_bn(M, N, g->nsm);
+  if (bn == 256) {
     if (epi == TC_EPI_BIAS) return launch<256, 2, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
     if (epi == TC_EPI_BIAS_RELU) return launch<256, 2, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
     return launch<256, 2, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
+  }
+  if (bn == 64) {
+    if (epi == TC_EPI_BIAS) return launch<64, 4, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
+    if (epi == TC_EPI_BIAS_RELU) return launch<64, 4, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
+    return launch<64, 4, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
   }
   if (epi == TC_EPI_BIAS) return launch<128, 3, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
   if (epi == TC_EPI_BIAS_RELU) return launch<128, 3, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);

@@ -16,7 +16,8 @@ bool tc_gemm_supported(int M, int N, int K);
 // (ReLU mask source); DT optional [N][t_rows] transposed copy of D's first t_rows rows.
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, const float* A,
                        const float* Bh, const float* Bl, const float* bias, const float* aux,
-                       int ldaux, float* D, float* DT, int t_rows);
+                       int ldaux, float* D, float* DT, int t_rows,
+                       unsigned long long* trace = nullptr);
 // Weight gradient: D[M][N] = A[M][K] . B[N][K]^T with both operands raw, split-K over K with a
 // deterministic reduction through ws (>= S * M * N floats).
 hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, const float* A,

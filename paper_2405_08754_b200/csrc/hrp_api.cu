@@ -1037,6 +1037,28 @@ hrp_status hrp_set_weights(hrp_ctx* c, const float* in) {
   return HRP_OK;
 }
 
+hrp_status hrp_diag_gemm(int device, void* cuda_stream, int M, int N, int K, const float* d_A,
+                         const float* d_W, const float* d_bias, float* d_D, uint64_t* d_trace) {
+  if (!d_A || !d_W || !d_bias || !d_D) return fail(HRP_EINVAL, "NULL argument");
+  if (!tc_gemm_supported(M, N, K)) return fail(HRP_ERANGE, "shape not supported (K % 4)");
+  CK(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  TcGemm* g = nullptr;
+  hrp_status s = tc_gemm_create(&g, device, M, nullptr, 0);
+  if (s) return fail(s, tc_gemm_error());
+  float* split = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&split, sizeof(float) * 2 * (size_t)N * K, st);
+  if (e != cudaSuccess) { tc_gemm_destroy(g); return fail(HRP_ENOMEM, cudaGetErrorString(e)); }
+  s = tc_split(g, st, N, K, d_W, split, split + (size_t)N * K, nullptr, nullptr);
+  if (!s)
+    s = tc_gemm_run(g, st, TC_EPI_BIAS, M, N, K, d_A, split, split + (size_t)N * K, d_bias,
+                    nullptr, 0, d_D, nullptr, 0, reinterpret_cast<unsigned long long*>(d_trace));
+  cudaFreeAsync(split, st);
+  tc_gemm_destroy(g);
+  if (s) return fail(s, tc_gemm_error());
+  return HRP_OK;
+}
+
 hrp_status hrp_sync(hrp_ctx* c) {
   if (!c) return fail(HRP_EINVAL, "NULL argument");
   CK(cudaSetDevice(c->device));

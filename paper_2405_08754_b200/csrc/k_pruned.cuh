@@ -91,33 +91,115 @@ __device__ __forceinline__ int64_t Fj(const DevSpace& sp, const float* z, const 
   return fixed_point(z[1 + sp.L + j * sp.T + t] - meanJ[t]);
 }
 
+// Leaf of the assignment search: jobs j[k] on slots k of layout l with score v.
+template <int C>
+__device__ __forceinline__ void pleaf(const PTabs& tb, int l, int W, const int (&js)[4], int64_t v,
+                                      int64_t& best, int64_t& bidx) {
+  // group g = sorted jobs; sigma(i) = slot of member g_i; index = off + rank(g) C! + lehmer
+  int g[4], sg[4];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    int r = 0;
+#pragma unroll
+    for (int i2 = 0; i2 < C; ++i2) r += js[i2] < js[i];
+    g[r] = js[i];
+    sg[r] = i;
+  }
+  int64_t rk = 0;
+  int prev = -1;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    rk += c_binom[W - 1 - prev][C - i] - c_binom[W - g[i]][C - i];
+    prev = g[i];
+  }
+  int lc = 0;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    int d = 0;
+#pragma unroll
+    for (int i2 = i + 1; i2 < C; ++i2) d += sg[i2] < sg[i];
+    lc += d * (C - 1 - i == 3 ? 6 : C - 1 - i == 2 ? 2 : 1);
+  }
+  constexpr int64_t fC = C == 1 ? 1 : C == 2 ? 2 : C == 3 ? 6 : 24;
+  const int64_t idx = tb.off[l] + rk * fC + lc;
+  if (v > best || idx < bidx) { best = v; bidx = idx; }
+}
+
+// Depth-first search over the C^C Top-list assignments of one layout, values descending per
+// slot, with the bound "partial + best remaining < best => stop this level" (lists sorted).
+template <int C>
+__device__ __forceinline__ void psearch(const PTabs& tb, const PWarpSmem& w, int l, int W,
+                                        uint32_t ty, int64_t base, int64_t& best, int64_t& bidx,
+                                        int64_t& nevals) {
+  int tk[4];
+#pragma unroll
+  for (int k = 0; k < C; ++k) tk[k] = (ty >> (8 * k)) & 255;
+#pragma unroll
+  for (int k = 0; k < C; ++k)
+    if (w.top[tk[k] * 4 + C - 1] < 0) return;  // fewer than C unscheduled jobs
+  int64_t ub[5];
+  ub[C] = 0;
+#pragma unroll
+  for (int k = C - 1; k >= 0; --k) ub[k] = ub[k + 1] + w.topv[tk[k] * 4];
+  int js[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int q0 = 0; q0 < C; ++q0) {
+    js[0] = w.top[tk[0] * 4 + q0];
+    const int64_t v0 = base + w.topv[tk[0] * 4 + q0];
+    if (v0 + ub[1] < best) break;
+    if (C == 1) { ++nevals; if (v0 >= best) pleaf<C>(tb, l, W, js, v0, best, bidx); continue; }
+#pragma unroll
+    for (int q1 = 0; q1 < (C > 1 ? C : 1); ++q1) {
+      js[1] = w.top[tk[1] * 4 + q1];
+      const int64_t v1 = v0 + w.topv[tk[1] * 4 + q1];
+      if (v1 + ub[2] < best) break;
+      if (js[1] == js[0]) continue;
+      if (C == 2) { ++nevals; if (v1 >= best) pleaf<C>(tb, l, W, js, v1, best, bidx); continue; }
+#pragma unroll
+      for (int q2 = 0; q2 < (C > 2 ? C : 1); ++q2) {
+        js[2] = w.top[tk[2] * 4 + q2];
+        const int64_t v2 = v1 + w.topv[tk[2] * 4 + q2];
+        if (v2 + ub[3] < best) break;
+        if (js[2] == js[0] || js[2] == js[1]) continue;
+        if (C == 3) { ++nevals; if (v2 >= best) pleaf<C>(tb, l, W, js, v2, best, bidx); continue; }
+#pragma unroll
+        for (int q3 = 0; q3 < (C > 3 ? C : 1); ++q3) {
+          js[3] = w.top[tk[3] * 4 + q3];
+          const int64_t v3 = v2 + w.topv[tk[3] * 4 + q3];
+          if (v3 + ub[4] < best) break;
+          if (js[3] == js[0] || js[3] == js[1] || js[3] == js[2]) continue;
+          ++nevals;
+          if (v3 >= best) pleaf<C>(tb, l, W, js, v3, best, bidx);
+        }
+      }
+    }
+  }
+}
+
 // Greedy (exact pruned) argmax of one state by one warp.  Returns (best, bidx) in all lanes;
 // bidx = INT64_MAX when no action is valid.
 __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
                                     const float* __restrict__ z, float meanL, uint64_t sched,
                                     int64_t& best, int64_t& bidx, int64_t& nevals) {
   const int lane = threadIdx.x & 31;
-  const int W = sp.W, T = sp.T, cm = sp.cmax;
+  const int W = sp.W, T = sp.T;
+  const float* aJ = z + 1 + sp.L;
   for (int t = lane; t < T; t += 32) {
-    int64_t bv[4] = {INT64_MIN, INT64_MIN, INT64_MIN, INT64_MIN};
-    int bj[4] = {-1, -1, -1, -1};
+    // top-4 by (value desc, position asc): register-only insertion network
+    int64_t b0 = INT64_MIN, b1 = INT64_MIN, b2 = INT64_MIN, b3 = INT64_MIN;
+    int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
+    const float mj = w.meanJ[t];
     for (int j = 0; j < W; ++j) {
       if ((sched >> j) & 1ull) continue;
-      const int64_t v = Fj(sp, z, w.meanJ, j, t);
-      if (v <= bv[cm - 1]) continue;  // strictly better than the current last (ties keep lower j)
-      int pos = cm - 1;
-      while (pos > 0 && bv[pos - 1] < v) {
-        bv[pos] = bv[pos - 1];
-        bj[pos] = bj[pos - 1];
-        --pos;
-      }
-      bv[pos] = v;
-      bj[pos] = j;
+      const int64_t v = fixed_point(aJ[j * T + t] - mj);
+      if (v <= b3) continue;  // ties keep the lower position
+      b3 = v; j3 = j;
+      if (b3 > b2) { int64_t x = b2; b2 = b3; b3 = x; int y = j2; j2 = j3; j3 = y; }
+      if (b2 > b1) { int64_t x = b1; b1 = b2; b2 = x; int y = j1; j1 = j2; j2 = y; }
+      if (b1 > b0) { int64_t x = b0; b0 = b1; b1 = x; int y = j0; j0 = j1; j1 = y; }
     }
-    for (int q = 0; q < 4; ++q) {
-      w.top[t * 4 + q] = bj[q];
-      w.topv[t * 4 + q] = bv[q];
-    }
+    w.top[t * 4 + 0] = j0; w.top[t * 4 + 1] = j1; w.top[t * 4 + 2] = j2; w.top[t * 4 + 3] = j3;
+    w.topv[t * 4 + 0] = b0; w.topv[t * 4 + 1] = b1; w.topv[t * 4 + 2] = b2; w.topv[t * 4 + 3] = b3;
   }
   __syncwarp();
   const int64_t Fv = fixed_point(z[0]);
@@ -126,60 +208,11 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   for (int l = lane; l < sp.L; l += 32) {
     const int C = tb.nsl[l];
     const uint32_t ty = tb.stype[l];
-    int tk[4];
-    bool ok = true;
-    for (int k = 0; k < C; ++k) {
-      tk[k] = (ty >> (8 * k)) & 255;
-      if (w.top[tk[k] * 4 + C - 1] < 0) ok = false;  // fewer than C unscheduled jobs
-    }
-    if (!ok) continue;
     const int64_t base = Fv + fixed_point(z[1 + l] - meanL);
-    int64_t ub[5];
-    ub[C] = 0;
-    for (int k = C - 1; k >= 0; --k) ub[k] = ub[k + 1] + w.topv[tk[k] * 4];
-    int q[4] = {0, 0, 0, 0};
-    int js[4];
-    int64_t part[5];
-    part[0] = base;
-    int k = 0;
-    // iterative DFS over slot k choosing q[k] in 0..C-1 (values descending)
-    while (k >= 0) {
-      if (q[k] >= C) {  // exhausted this level
-        q[k] = 0;
-        --k;
-        if (k >= 0) ++q[k];
-        continue;
-      }
-      const int j = w.top[tk[k] * 4 + q[k]];
-      const int64_t v = part[k] + w.topv[tk[k] * 4 + q[k]];
-      if (v + ub[k + 1] < best) {  // sorted: later choices at this level are no better
-        q[k] = C;
-        continue;
-      }
-      bool dup = false;
-      for (int i = 0; i < k; ++i) dup |= js[i] == j;
-      if (dup) { ++q[k]; continue; }
-      js[k] = j;
-      if (k == C - 1) {
-        ++nevals;
-        if (v >= best) {
-          int g[4], sg[4];
-          for (int i = 0; i < C; ++i) {
-            int r = 0;
-            for (int i2 = 0; i2 < C; ++i2) r += js[i2] < js[i];
-            g[r] = js[i];
-            sg[r] = i;
-          }
-          const int64_t idx = tb.off[l] + rank_comb(g, C, W) * c_fact[C] + lehmer(sg, C);
-          if (v > best || idx < bidx) { best = v; bidx = idx; }
-        }
-        ++q[k];
-      } else {
-        part[k + 1] = v;
-        ++k;
-        q[k] = 0;
-      }
-    }
+    if (C == 1) psearch<1>(tb, w, l, W, ty, base, best, bidx, nevals);
+    else if (C == 2) psearch<2>(tb, w, l, W, ty, base, best, bidx, nevals);
+    else if (C == 3) psearch<3>(tb, w, l, W, ty, base, best, bidx, nevals);
+    else psearch<4>(tb, w, l, W, ty, base, best, bidx, nevals);
   }
   warp_best(best, bidx);
 }
