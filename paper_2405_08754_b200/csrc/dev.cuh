@@ -7,6 +7,8 @@ namespace hrp {
 
 constexpr int kThreads = 256;
 
+__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
 // Layout space on the device (passed by value; arrays live in global memory).
 struct DevSpace {
   int W, cmax, L, T, H, q3;

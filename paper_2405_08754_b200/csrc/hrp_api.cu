@@ -17,10 +17,20 @@
 #include "k_gemm_simt.cuh"
 #include "k_env.cuh"
 #include "k_brute.cuh"
-#include "k_pruned.cuh"
+#include "k_select.cuh"
 #include "gemm_tc.h"
 
 using namespace hrp;
+
+// Instantiate F(X) for the selection-kernel variant v (0 pruned, 1..4 explicit, Cmax = v).
+#define HRP_VARIANT(v, F) \
+  switch (v) {            \
+    case 0: F(0); break;  \
+    case 1: F(1); break;  \
+    case 2: F(2); break;  \
+    case 3: F(3); break;  \
+    default: F(4); break; \
+  }
 
 namespace {
 
@@ -247,10 +257,9 @@ struct hrp_ctx {
   float* dsq = nullptr;
   int64_t* tmp_i64 = nullptr;         // [rows]
   unsigned long long* n_evals = nullptr;
-  size_t sel_smem = 0;
-  size_t p_smem = 0;   // pruned warp-per-state kernels
+  size_t p_smem = 0;   // warp-per-state selection / TD kernels
+  int sel_variant = 0; // 0 pruned argmax, 1..4 explicit enumeration with Cmax = variant
   int p_grid = 0;
-  int sel_grid = 0;
   int64_t launches = 0;
   TcGemm* tc = nullptr;
   // per-kernel device timing (hrp_profile)
@@ -510,13 +519,10 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.explicit_mode = c->explicit_mode;
   a.n_evals = c->n_evals;
   prof_begin(c);
-  if (c->explicit_mode) {
-    const int grid = std::min(a.M, c->sel_grid);
-    select_kernel<<<grid, kThreads, c->sel_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
-  } else {
-    const int grid = std::min((a.M + kPWarps - 1) / kPWarps, c->p_grid);
-    pwarp_select_kernel<<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a);
-  }
+  const int grid = std::min((a.M + kPWarps - 1) / kPWarps, c->p_grid);
+#define HRP_SEL(X) sel_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
+  HRP_VARIANT(c->sel_variant, HRP_SEL);
+#undef HRP_SEL
   return launch_check(c, HRP_K_SELECT);
 }
 
@@ -652,10 +658,10 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   int nsm = 148;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   // argmax mode: explicit enumeration of every action needs the group tables (W <= 16)
-  if (cfg->argmax_mode == 1 && hs.W > 16) return fail(HRP_ERANGE, "explicit argmax needs W <= 16");
-  c->explicit_mode = cfg->argmax_mode == 1 || (cfg->argmax_mode == 0 && hs.W <= 16);
+  if (cfg->argmax_mode == 1 && hs.W > kXMaxW) return fail(HRP_ERANGE, "explicit argmax needs W <= 16");
+  c->explicit_mode = cfg->argmax_mode == 1 || (cfg->argmax_mode == 0 && hs.W <= kXMaxW);
   c->gemm_mode = cfg->gemm_mode == 0 ? 2 : cfg->gemm_mode;
-  if ((s = upload_tables(hs, prof, c->explicit_mode, c->ar, c->stream, c->dt))) return s;
+  if ((s = upload_tables(hs, prof, false, c->ar, c->stream, c->dt))) return s;
   // network dims and flat parameter layout (W [out][in] then b [out] per layer)
   c->dims.push_back(hs.W * kRowIn);
   for (int i = 0; i < cfg->hidden_layers; ++i) c->dims.push_back(cfg->hidden_width);
@@ -733,32 +739,33 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     CK(cudaMemsetAsync(c->theta, 0, sizeof(float) * o, c->stream));
     CK(cudaMemsetAsync(c->theta_t, 0, sizeof(float) * o, c->stream));
   }
-  // selection kernel launch shape
-  c->sel_smem = select_smem_bytes(hs.L, W, hs.T, H, hs.cmax, c->dt.sp.ncombo, c->explicit_mode);
-  if (c->sel_smem > 227 * 1024) return fail(HRP_ERANGE, "selection tables exceed shared memory");
+  // selection / TD kernel launch shape (warp per state)
+  c->p_smem = pwarp_smem_bytes(hs.L, hs.T, c->explicit_mode);
+  if (c->p_smem > 227 * 1024) return fail(HRP_ERANGE, "selection tables exceed shared memory");
   {
     // the attribute is per function (process-wide): keep the largest any context needs
-    static int sel_smem_max[64] = {0};
-    int& mx = sel_smem_max[device & 63];
-    if ((int)c->sel_smem > mx) {
-      CK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
-      CK(cudaFuncSetAttribute(td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->sel_smem));
-      mx = (int)c->sel_smem;
+    static int p_smem_max[64] = {0};
+    if ((int)c->p_smem > p_smem_max[device & 63]) {
+      const int b = (int)c->p_smem;
+#define HRP_ATTR(X)                                                                          \
+  do {                                                                                       \
+    CK(cudaFuncSetAttribute(sel_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, b)); \
+    CK(cudaFuncSetAttribute(td_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));  \
+  } while (0)
+      HRP_ATTR(0); HRP_ATTR(1); HRP_ATTR(2); HRP_ATTR(3); HRP_ATTR(4);
+#undef HRP_ATTR
+      p_smem_max[device & 63] = b;
     }
   }
   int occ = 1;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_kernel, kThreads, c->sel_smem));
-  c->sel_grid = nsm * std::max(1, occ);
-  c->p_smem = pwarp_smem_bytes(hs.L, hs.T);
+  c->sel_variant = c->explicit_mode ? hs.cmax : 0;
   {
-    static int p_smem_max[64] = {0};
-    if ((int)c->p_smem > p_smem_max[device & 63]) {
-      CK(cudaFuncSetAttribute(pwarp_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem));
-      CK(cudaFuncSetAttribute(pwarp_td_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->p_smem));
-      p_smem_max[device & 63] = (int)c->p_smem;
-    }
+    cudaError_t e = cudaSuccess;
+#define HRP_OCC(X) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sel_kernel<X>, kPWarps * 32, c->p_smem)
+    HRP_VARIANT(c->sel_variant, HRP_OCC);
+#undef HRP_OCC
+    CK(e);
   }
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pwarp_select_kernel, kPWarps * 32, c->p_smem));
   c->p_grid = nsm * std::max(1, occ);
   if (c->gemm_mode == 2) {
     if ((s = tc_gemm_create(&c->tc, device, (int)R, c->dims.data(), (int)c->dims.size()))) {
@@ -908,11 +915,12 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.astar = d_astar;
   t.n_evals = c->n_evals;
   prof_begin(c);
-  if (c->explicit_mode)
-    td_kernel<<<std::min(B, c->sel_grid), kThreads, c->sel_smem, c->stream>>>(c->dt.sp, t);
-  else
-    pwarp_td_kernel<<<std::min((B + kPWarps - 1) / kPWarps, c->p_grid), kPWarps * 32, c->p_smem,
-                      c->stream>>>(c->dt.sp, t);
+  {
+    const int grid = std::min((B + kPWarps - 1) / kPWarps, c->p_grid);
+#define HRP_TD(X) td_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, t)
+    HRP_VARIANT(c->sel_variant, HRP_TD);
+#undef HRP_TD
+  }
   if ((s = launch_check(c, HRP_K_TD))) return s;
   prof_begin(c);
   loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);

@@ -1,30 +1,78 @@
-// Warp-per-state kernels for the exact top-C pruned argmax (reading R15):
-//   pwarp_select_kernel  a4-a7 fused (centering, fixed point, greedy argmax, epsilon-greedy,
-//                        co-run reward, transition, replay insert, auto-reset) or inference
-//   pwarp_td_kernel      a9-a10 (double-DQN target argmax on s', target Q, TD error, loss
-//                        term, structured head gradient)
+// Warp-per-state selection kernels of libhrp (sm_100a):
+//   sel_kernel<X>  (X = 0: pruned argmax; X = 1..4: explicit enumeration with Cmax = X)
+//                  a4-a7 fused: duelling centering + fixed point (R15, R20), greedy
+//                  argmax, epsilon-greedy (R14), co-run reward (P:122, P:139-140,
+//                  Table VI, R7-R9), transition + replay insert + auto-reset
+//                  (R19); or inference (epsilon = 0)
+//   td_kernel<X>   a9-a10: double-DQN target argmax on s', target Q, TD error, loss
+//                  term, structured head gradient of (1/2) delta^2
 // One warp owns one state at a time; no block-wide barriers.  The head row z is read from
-// global memory (L2-resident, coalesced across lanes); per warp only the slot-type means and
-// the Top-C lists live in shared memory.
+// global memory (L2-resident, coalesced across lanes).  Two exact greedy argmax algorithms:
 //
-// Exactness: Top_tau = the C best unscheduled positions by (F(cJ[j][tau]) desc, j asc); any
-// lowest-index maximiser uses only Top-list jobs (exchange argument, oracle/pruned.py).  Per
-// layout the <= C^C assignments are searched depth-first in descending-value order with the
-// bound "partial + sum of the remaining slots' best < best so far => stop" -- valid because
-// the lists are sorted, and ties (== best) are still visited so the lowest index wins.
+// X = Cmax >= 1, explicit enumeration ("score every valid action", W <= 16):
+//   lane <-> layout (32 layouts with the same slot count C per pass).  Every lane walks the
+//   same lexicographic sequence of C-subsets {r_0 < .. < r_{C-1}} of the U free window
+//   positions (loops are warp-uniform) and scores all C! slot assignments of each subset with
+//   fp32 prefix sums shared between permutations: level k of the loop nest loads row r_k's C
+//   values cJ[r_k][tau(slot)] and extends the P(C, k) partial sums to P(C, k + 1).
+//   Filter + exact verification: an fp32 score s~ differs from the exact fixed-point score
+//   Q^ / 2^32 by at most delta = 2^-20 S + 2^-29, S = |v| + max|cL| + Cmax max|cJ| (at most
+//   C + 1 fp32 roundings of relative 2^-24 each, plus 2^-33 per F rounding).  The exact
+//   lowest-index maximiser a* therefore has s~(a*) >= rm - 2 delta for any running maximum rm
+//   of s~, so every action with s~ >= rm - 2 delta is re-scored exactly (int64 Q^ and its
+//   action index) and the (Q^ desc, idx asc) maximum over those is the argmax over all valid
+//   actions -- identical to scoring every action in int64.
+//
+// X = 0, exact top-C pruning (any W <= 64): Top_tau = the C best unscheduled
+//   positions by (F(cJ[j][tau]) desc, j asc); any lowest-index maximiser uses only Top-list
+//   jobs (exchange argument, oracle/pruned.py).  Per layout the <= C^C assignments are searched
+//   depth-first in descending-value order with the bound "partial + sum of the remaining slots'
+//   best < best so far => stop" (lists sorted; ties are still visited so the lowest index wins).
 #pragma once
+#include <float.h>
 #include "dev.cuh"
 #include "k_env.cuh"
 
 namespace hrp {
 
-constexpr int kPWarps = 8;  // warps (states in flight) per CTA
+constexpr int kPWarps = 8;   // warps (states in flight) per CTA
+constexpr int kXMaxW = 16;   // explicit enumeration: window size limit
+
+__host__ __device__ constexpr int xstride(int T) { return T | 1; }  // odd: conflict-free rows
 
 struct PWarpSmem {
-  float* meanJ;       // [T]
-  int* top;           // [T][4] positions
-  int64_t* topv;      // [T][4] F values
+  float* meanJ;   // [T] slot-type means of the job advantages
+  int* top;       // pruned: [T][4] Top-C positions
+  int64_t* topv;  // pruned: [T][4] their F values
+  float* cj;      // explicit: [U][xstride(T)] centred job advantages of the free positions
+  int* pos;       // explicit: [U] free window positions, ascending
 };
+
+struct PTabs {
+  int64_t* off;        // [L+1] action offsets
+  uint32_t* stype;     // [L] slot type ids (4 x u8)
+  uint8_t* nsl;        // [L] slot count C
+  uint16_t* lay_of_c;  // [L] layouts grouped by C (C ascending, layout order inside)
+  int cstart[6];       // lay_of_c offsets per C
+};
+
+__host__ __device__ inline size_t pwarp_bytes(int T, bool x) {
+  size_t b = align16(sizeof(float) * T);
+  if (x)
+    b += align16(sizeof(float) * kXMaxW * xstride(T)) + align16(sizeof(int) * kXMaxW);
+  else
+    b += align16(sizeof(int) * T * 4) + align16(sizeof(int64_t) * T * 4);
+  return b;
+}
+
+__host__ __device__ inline size_t ptabs_bytes(int L) {
+  return align16(sizeof(int64_t) * (L + 1)) + align16(sizeof(uint32_t) * L) + align16(L) +
+         align16(sizeof(uint16_t) * L);
+}
+
+__host__ __device__ inline size_t pwarp_smem_bytes(int L, int T, bool x) {
+  return ptabs_bytes(L) + kPWarps * pwarp_bytes(T, x);
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -32,19 +80,13 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-__host__ __device__ inline size_t pwarp_smem_bytes(int L, int T) {
-  size_t per_warp = align16(sizeof(float) * T) + align16(sizeof(int) * T * 4) +
-                    align16(sizeof(int64_t) * T * 4);
-  size_t tabs = align16(sizeof(int64_t) * (L + 1)) + align16(sizeof(uint32_t) * L) + align16(L);
-  return tabs + kPWarps * per_warp;
+__device__ __forceinline__ float warp_maxf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
-struct PTabs {
-  int64_t* off;
-  uint32_t* stype;
-  uint8_t* nsl;
-};
-
+template <int X>
 __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem& w) {
   PTabs t;
   size_t o = 0;
@@ -52,23 +94,45 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
   t.off = (int64_t*)take(sizeof(int64_t) * (sp.L + 1));
   t.stype = (uint32_t*)take(sizeof(uint32_t) * sp.L);
   t.nsl = (uint8_t*)take(sp.L);
-  const int wi = threadIdx.x >> 5;
-  const size_t per_warp = align16(sizeof(float) * sp.T) + align16(sizeof(int) * sp.T * 4) +
-                          align16(sizeof(int64_t) * sp.T * 4);
-  uint8_t* wb = base + o + wi * per_warp;
+  t.lay_of_c = (uint16_t*)take(sizeof(uint16_t) * sp.L);
+  uint8_t* wb = base + o + (threadIdx.x >> 5) * pwarp_bytes(sp.T, X > 0);
   w.meanJ = (float*)wb;
-  w.top = (int*)(wb + align16(sizeof(float) * sp.T));
-  w.topv = (int64_t*)(wb + align16(sizeof(float) * sp.T) + align16(sizeof(int) * sp.T * 4));
+  wb += align16(sizeof(float) * sp.T);
+  w.top = nullptr;
+  w.topv = nullptr;
+  w.cj = nullptr;
+  w.pos = nullptr;
+  if (X > 0) {
+    w.cj = (float*)wb;
+    w.pos = (int*)(wb + align16(sizeof(float) * kXMaxW * xstride(sp.T)));
+  } else {
+    w.top = (int*)wb;
+    w.topv = (int64_t*)(wb + align16(sizeof(int) * sp.T * 4));
+  }
   for (int i = threadIdx.x; i <= sp.L; i += blockDim.x) t.off[i] = sp.off[i];
   for (int i = threadIdx.x; i < sp.L; i += blockDim.x) {
     t.stype[i] = sp.lay_stype[i];
     t.nsl[i] = sp.lay_n[i];
   }
+  int k = 0;
+  for (int C = 1; C <= 4; ++C) {
+    t.cstart[C] = k;
+    k += sp.nlay_c[C];
+  }
+  t.cstart[0] = 0;
+  t.cstart[5] = k;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int q = 0;
+    for (int C = 1; C <= 4; ++C)
+      for (int l = 0; l < sp.L; ++l)
+        if (t.nsl[l] == C) t.lay_of_c[q++] = (uint16_t)l;
+  }
   __syncthreads();
   return t;
 }
 
-// Means of a head row (global z): returns meanL, fills meanJ[T] (warp-local smem).
+// Means of a head row (global z): returns meanL, fills meanJ[T] (warp-local smem) (R20).
 __device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict__ z, float* meanJ) {
   const int lane = threadIdx.x & 31;
   __syncwarp();  // previous readers of meanJ are done
@@ -90,6 +154,181 @@ __device__ __forceinline__ int64_t Fj(const DevSpace& sp, const float* z, const 
                                       int t) {
   return fixed_point(z[1 + sp.L + j * sp.T + t] - meanJ[t]);
 }
+
+// ---------------------------------------------------------------------------------------
+// Explicit enumeration (X = true)
+
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3 (sm_100)
+  return r;
+}
+
+template <int N>
+__device__ __forceinline__ float vmax(const float (&s)[N]) {
+  if constexpr (N == 1) {
+    return s[0];
+  } else if constexpr (N == 2) {
+    return fmaxf(s[0], s[1]);
+  } else {
+    constexpr int M = (N + 2) / 3;
+    float t[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      if (3 * i + 2 < N) t[i] = fmax3f(s[3 * i], s[3 * i + 1], s[3 * i + 2]);
+      else if (3 * i + 1 < N) t[i] = fmaxf(s[3 * i], s[3 * i + 1]);
+      else t[i] = s[3 * i];
+    }
+    return vmax<M>(t);
+  }
+}
+
+struct XState {
+  const float* cj;  // [U][stride]
+  const int* pos;   // [U]
+  int stride, U, W;
+  float thr, rm, two_delta;
+  int64_t best, bidx;
+  int t[4];         // this lane's layout: slot types
+  int64_t base_f;   // F(v) + F(cL[l])
+  int64_t off;      // off[l]
+};
+
+// Exact re-scoring of the permutations of subset r whose fp32 score passed the filter.
+template <int C>
+__device__ __forceinline__ void xverify(XState& x, const int (&r)[4], const float (&S)[fact_c(C)],
+                                        float mx) {
+  int g[4];
+#pragma unroll
+  for (int i = 0; i < C; ++i) g[i] = x.pos[r[i]];
+  const int64_t idx0 = x.off + rank_comb(g, C, x.W) * fact_c(C);
+#pragma unroll
+  for (int p = 0; p < fact_c(C); ++p) {
+    if (S[p] >= x.thr) {
+      int64_t q = x.base_f;
+#pragma unroll
+      for (int i = 0; i < C; ++i)
+        q += fixed_point(x.cj[r[i] * x.stride + x.t[perm_elem_c(C, p, i)]]);
+      const int64_t idx = idx0 + p;
+      if (q > x.best || (q == x.best && idx < x.bidx)) {
+        x.best = q;
+        x.bidx = idx;
+      }
+    }
+  }
+  x.rm = fmaxf(x.rm, mx);
+  x.thr = x.rm - x.two_delta;
+}
+
+// Level K of the subset loop nest: Sp holds the P(C, K) prefix sums (Lehmer order of the
+// length-K permutation prefixes); row r_K extends them to P(C, K + 1).
+template <int C, int K>
+__device__ __forceinline__ void xlevel(XState& x, int (&r)[4],
+                                       const float (&Sp)[fact_c(C) / fact_c(C - K)], int r_lo) {
+  constexpr int NQ = fact_c(C) / fact_c(C - K - 1);
+  const int r_hi = x.U - (C - K);
+#pragma unroll 1
+  for (int rr = r_lo; rr <= r_hi; ++rr) {
+    r[K] = rr;
+    const float* row = x.cj + rr * x.stride;
+    float m[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) m[k] = row[x.t[k]];  // C LDS (row broadcast, odd stride)
+    float S[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      S[q] = Sp[q / (C - K)] + m[perm_elem_c(C, q * fact_c(C - K - 1), K)];
+    if constexpr (K + 1 == C) {
+      const float mx = vmax<NQ>(S);
+      if (mx >= x.thr) xverify<C>(x, r, S, mx);
+    } else {
+      xlevel<C, K + 1>(x, r, S, rr + 1);
+    }
+    if constexpr (K == 0 && C > 1) {
+      // share the running maximum across the warp (any lane's rm is a valid bound)
+      x.rm = warp_maxf(x.rm);
+      x.thr = x.rm - x.two_delta;
+    }
+  }
+}
+
+template <int C>
+__device__ __forceinline__ void xrun(XState& x, float base) {
+  const float S0[1] = {base};
+  int r[4] = {0, 0, 0, 0};
+  xlevel<C, 0>(x, r, S0, 0);
+}
+
+// Greedy argmax of one state by explicit enumeration of every valid action (slot counts up to
+// CM = Cmax).  Returns (best, bidx) in all lanes; bidx = INT64_MAX when no action is valid.
+template <int CM>
+__device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
+                               const float* __restrict__ z, float meanL, uint64_t sched,
+                               int64_t& best, int64_t& bidx, int64_t& nevals) {
+  const int lane = threadIdx.x & 31;
+  const int W = sp.W, T = sp.T, L = sp.L;
+  const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
+  const uint64_t freem = all & ~sched;
+  const int U = __popcll(freem);
+  const int stride = xstride(T);
+  __syncwarp();  // previous state's readers of cj / pos are done
+  if (lane < W && ((freem >> lane) & 1ull))
+    w.pos[__popcll(freem & ((1ull << lane) - 1ull))] = lane;
+  __syncwarp();
+  const float* aJ = z + 1 + L;
+  float amax = 0.f;
+  for (int i = lane; i < U * T; i += 32) {
+    const int rr = i / T, t = i - rr * T;
+    const float v = aJ[w.pos[rr] * T + t] - w.meanJ[t];
+    w.cj[rr * stride + t] = v;
+    amax = fmaxf(amax, fabsf(v));
+  }
+  float lmax = 0.f;
+  for (int l = lane; l < L; l += 32) lmax = fmaxf(lmax, fabsf(z[1 + l] - meanL));
+  amax = warp_maxf(amax);
+  lmax = warp_maxf(lmax);
+  __syncwarp();
+  const float v = z[0];
+  XState x;
+  x.cj = w.cj;
+  x.pos = w.pos;
+  x.stride = stride;
+  x.U = U;
+  x.W = W;
+  x.two_delta = 2.f * ((fabsf(v) + lmax + (float)sp.cmax * amax) * 0x1p-20f + 0x1p-29f);
+  x.rm = -FLT_MAX;
+  x.thr = -FLT_MAX;
+  x.best = INT64_MIN;
+  x.bidx = INT64_MAX;
+  const int64_t Fv = fixed_point(v);
+  for (int C = 1; C <= CM && C <= U; ++C) {
+    const int n = tb.cstart[C + 1] - tb.cstart[C];
+#pragma unroll 1
+    for (int p0 = 0; p0 < n; p0 += 32) {
+      const int li = p0 + lane;
+      const bool act = li < n;
+      const int l = tb.lay_of_c[tb.cstart[C] + (act ? li : 0)];
+      const uint32_t ty = tb.stype[l];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x.t[k] = (ty >> (8 * k)) & 255;
+      const float cl = z[1 + l] - meanL;
+      x.base_f = Fv + fixed_point(cl);
+      x.off = tb.off[l];
+      const float base = act ? v + cl : -INFINITY;  // idle lanes never pass the filter
+      if (C == 1) xrun<1>(x, base);
+      if constexpr (CM >= 2) if (C == 2) xrun<2>(x, base);
+      if constexpr (CM >= 3) if (C == 3) xrun<3>(x, base);
+      if constexpr (CM >= 4) if (C == 4) xrun<4>(x, base);
+    }
+  }
+  if (lane == 0) nevals += n_valid(sp, sched);
+  best = x.best;
+  bidx = x.bidx;
+  warp_best(best, bidx);
+}
+
+// ---------------------------------------------------------------------------------------
+// Exact top-C pruned search (X = false)
 
 // Leaf of the assignment search: jobs j[k] on slots k of layout l with score v.
 template <int C>
@@ -142,20 +381,20 @@ __device__ __forceinline__ void psearch(const PTabs& tb, const PWarpSmem& w, int
 #pragma unroll
   for (int k = C - 1; k >= 0; --k) ub[k] = ub[k + 1] + w.topv[tk[k] * 4];
   int js[4] = {0, 0, 0, 0};
-#pragma unroll
+#pragma unroll 1
   for (int q0 = 0; q0 < C; ++q0) {
     js[0] = w.top[tk[0] * 4 + q0];
     const int64_t v0 = base + w.topv[tk[0] * 4 + q0];
     if (v0 + ub[1] < best) break;
     if (C == 1) { ++nevals; if (v0 >= best) pleaf<C>(tb, l, W, js, v0, best, bidx); continue; }
-#pragma unroll
+#pragma unroll 1
     for (int q1 = 0; q1 < (C > 1 ? C : 1); ++q1) {
       js[1] = w.top[tk[1] * 4 + q1];
       const int64_t v1 = v0 + w.topv[tk[1] * 4 + q1];
       if (v1 + ub[2] < best) break;
       if (js[1] == js[0]) continue;
       if (C == 2) { ++nevals; if (v1 >= best) pleaf<C>(tb, l, W, js, v1, best, bidx); continue; }
-#pragma unroll
+#pragma unroll 1
       for (int q2 = 0; q2 < (C > 2 ? C : 1); ++q2) {
         js[2] = w.top[tk[2] * 4 + q2];
         const int64_t v2 = v1 + w.topv[tk[2] * 4 + q2];
@@ -217,6 +456,14 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   warp_best(best, bidx);
 }
 
+template <int X>
+__device__ __forceinline__ void greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
+                                       const float* __restrict__ z, float meanL, uint64_t sched,
+                                       int64_t& best, int64_t& bidx, int64_t& nevals) {
+  if constexpr (X > 0) xgreedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+  else pwarp_greedy(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+}
+
 // k-th valid action (index order), warp-parallel over layouts.
 __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, uint64_t sched,
                                           int64_t k) {
@@ -266,11 +513,12 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
   return -1;
 }
 
+template <int X>
 __global__ void __launch_bounds__(kPWarps * 32)
-pwarp_select_kernel(DevSpace sp, DevPool pool, SelArgs a) {
+sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
-  PTabs tb = pload_tabs(sp, smem_raw, w);
+  PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * kPWarps + (threadIdx.x >> 5);
   const int nw = gridDim.x * kPWarps;
@@ -281,7 +529,7 @@ pwarp_select_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     const uint64_t sched = a.sched[row];
     const float meanL = pwarp_means(sp, z, w.meanJ);
     int64_t best, bidx;
-    pwarp_greedy(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+    greedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
     if (a.mode == SEL_INFER) {
       if (lane == 0) {
         a.actions[row] = bidx == INT64_MAX ? -1 : bidx;
@@ -381,10 +629,11 @@ __device__ inline float pwarp_qfloat(const DevSpace& sp, const PTabs& tb, PWarpS
   return q;
 }
 
-__global__ void __launch_bounds__(kPWarps * 32) pwarp_td_kernel(DevSpace sp, TdArgs a) {
+template <int X>
+__global__ void __launch_bounds__(kPWarps * 32) td_kernel(DevSpace sp, TdArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
-  PTabs tb = pload_tabs(sp, smem_raw, w);
+  PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * kPWarps + (threadIdx.x >> 5);
   const int nw = gridDim.x * kPWarps;
@@ -398,7 +647,7 @@ __global__ void __launch_bounds__(kPWarps * 32) pwarp_td_kernel(DevSpace sp, TdA
       const float* zn = a.z_all + (size_t)(a.B + b) * H;
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
-      pwarp_greedy(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
+      greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
       const float qt = pwarp_qfloat(sp, tb, w, a.z_tgt + (size_t)b * H, astar, nullptr, nullptr,
                                     nullptr);
       y = a.br[b] + a.gamma * qt;
