@@ -177,13 +177,8 @@ def run_gpu(args, cfg):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    nccl_id = None
-    if world > 1:
-        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            buf.copy_(torch.frombuffer(bytearray(hrp.hrp_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(buf, 0)
-        nccl_id = bytes(buf.cpu().numpy().tobytes())
+    from paper_2405_08754_b200 import parallel
+    nccl_id = parallel.nccl_unique_id(dev) if world > 1 else None
     pool = synth.make_pool(cfg.pool)
     sc = cfg.space
     stream = torch.cuda.Stream(dev)
@@ -196,10 +191,12 @@ def run_gpu(args, cfg):
         sess = Session(cfg, pool, init_weights=th, device=local, rank=rank, world=world,
                        nccl_id=nccl_id, argmax_mode=args.argmax, gemm_mode=args.gemm,
                        stream=stream)
-        sess.reset(synth.make_windows(pool, E, sc.window, rank=rank, first_env=rank * E))
+        sess.reset(synth.make_windows(pool, E, sc.window, rank=rank,
+                                       first_env=parallel.env_shard(E, rank)))
     total = args.warmup + args.steps
     # per-step host streams, resident in HBM before the timed region
-    streams_h = [synth.step_streams(t, E, B, sc.window, pool, rank=rank, first_env=rank * E)
+    streams_h = [synth.step_streams(t, E, B, sc.window, pool, rank=rank,
+                                    first_env=parallel.env_shard(E, rank))
                  for t in range(total)]
     streams_d = [streams_to_dev(s, dev) for s in streams_h]
     thr = [synth.eps_threshold(t, cfg.n_decay) for t in range(total)]
@@ -219,7 +216,7 @@ def run_gpu(args, cfg):
         ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         n_launch0 = sess.launches()
-        evals0 = hrp.hrp_eval_count(sess.ctx)
+        evals0 = hrp.hrp_eval_counts(sess.ctx)
         clocks = Clocks(local)
         hrp.hrp_profile(sess.ctx, True)
         for k in range(args.steps):
@@ -233,13 +230,12 @@ def run_gpu(args, cfg):
         prof = hrp.hrp_profile_read(sess.ctx)
         hrp.hrp_profile(sess.ctx, False)
         n_launch = sess.launches() - n_launch0
-        evals = hrp.hrp_eval_count(sess.ctx) - evals0
+        evals1 = hrp.hrp_eval_counts(sess.ctx)
+        evals_k = (evals1[0] - evals0[0], evals1[1] - evals0[1])
+        evals = evals_k[0] + evals_k[1]
         ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
     # max over ranks
-    t_all = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
-    ms = float(t_all.item())
+    ms = parallel.max_over_ranks(ms, dev)
     value = world * E * args.steps / (ms / 1e3)
 
     # ---- e2e: host pinned streams copied in, results copied out, inside the timed region
@@ -260,24 +256,22 @@ def run_gpu(args, cfg):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        f0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        f1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         for k in range(args.steps):
             t = args.warmup + k
+            flush.zero_()                       # L2 flushed between timed steps, as above
+            f0[k].record(stream)
             for key, v in pinned[k].items():
                 bufs[key].copy_(v, non_blocking=True)
             one_step(t, bufs)
             out_h["actions"].copy_(sess.actions, non_blocking=True)
             out_h["rewards"].copy_(sess.rewards, non_blocking=True)
             out_h["loss"].copy_(sess.loss, non_blocking=True)
-        e1.record(stream)
+            f1[k].record(stream)
         stream.synchronize()
-        ms_e2e = e0.elapsed_time(e1)
-    te = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = world * E * args.steps / (float(te.item()) / 1e3)
+        ms_e2e = sum(a.elapsed_time(b) for a, b in zip(f0, f1))
+    e2e_value = world * E * args.steps / (parallel.max_over_ranks(ms_e2e, dev) / 1e3)
 
     if rank == 0:
         res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -297,7 +291,11 @@ def run_gpu(args, cfg):
                        "d2h_bytes_per_step": int(d2h)},
                "clocks": clk,
                "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
-        res["roofline"] = roofline(prof, args.steps, evals, cfg, osp, world)
+        rl = rooflines(prof, args.steps, evals_k, cfg, osp)
+        res["roofline"] = dominant(rl)
+        tot = sum(v["ms_per_step"] for v in rl.values())
+        res["roofline"]["share_of_step"] = rl[res["roofline"]["kernel"]]["ms_per_step"] / tot
+        res["rooflines"] = rl
         if not args.no_cpu_baseline and world == 1:
             res["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
         print(json.dumps(res), flush=True)
@@ -325,41 +323,68 @@ def sess_explicit(args, sc):
     return args.argmax == 1 or (args.argmax == 0 and sc.window <= 16)
 
 
-def roofline(prof, steps, evals, cfg, osp, world):
-    """Dominant kernel's achieved vs peak."""
-    peaks = {}
+def _peaks():
     try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
-        pass
-    top = max(prof.items(), key=lambda kv: kv[1][0])
-    name, (ms, cnt) = top
-    sec = ms / 1e3
-    clock = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    if name in ("select", "td"):
-        # ALU bound: algorithmic int32-lane ops = explicit Q^ evals x (2C + 2)
-        C = osp.cmax
-        ops = (evals / 2.0) * (2 * C + 2)   # select + td each hold ~half of the evals
-        peak = 148 * 128 * clock / 1e12    # Tops/s (lane-ops), 148 SMs x 128 lanes x f_max
-        ach = ops / sec / 1e12
-        return {"kernel": name, "bound": "alu", "achieved": ach, "peak": peak, "unit": "Tops/s",
-                "frac": ach / peak, "traffic": None,
-                "peak_src": "derived: 148 SM x 128 int32 lanes x sm_max_mhz (MEASURED_PEAKS)"}
-    if name.startswith("gemm"):
-        dims = [osp.W * 17] + [cfg.net.hidden_width] * cfg.net.hidden_layers + [osp.H]
-        F = sum(2 * dims[i] * dims[i + 1] for i in range(len(dims) - 1))
-        if name == "gemm_fwd":
-            flops = (cfg.n_envs + 3 * cfg.batch) * F * steps
-        else:
-            flops = cfg.batch * (2 * F - 2 * dims[0] * dims[1]) * steps
-        ach = flops / sec / 1e12
-        peak = float(peaks.get("bf16_tflops_sustained", 1407.2)) / 2.0  # tf32 = bf16 / 2
-        return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": peak,
-                "unit": "TFLOP/s", "frac": ach / peak, "traffic": None,
-                "peak_src": "MEASURED_PEAKS bf16_tflops_sustained x 1/2 (tf32 nominal ratio)"}
-    return {"kernel": name, "bound": "hbm", "achieved": None,
-            "peak": float(peaks.get("hbm_gbs", 6453.7)), "unit": "GB/s", "frac": None,
-            "traffic": None}
+        return {}
+
+
+def rooflines(prof, steps, evals, cfg, osp):
+    """Per kernel class: achieved vs peak.  `evals` = (select, td)
+    explicit Q-evaluations over the timed steps; prof = {class: (ms, launches)}."""
+    pk = _peaks()
+    clock = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    alu_peak = 148 * 128 * clock / 1e12                     # T lane-ops/s
+    tf32 = float(pk.get("bf16_tflops_sustained", 1407.2)) / 2.0
+    fp32_tc = tf32 / 3.0                                    # 3xTF32: three MMAs per product
+    hbm = float(pk.get("hbm_gbs", 6453.7))
+    dims = [osp.W * 17] + [cfg.net.hidden_width] * cfg.net.hidden_layers + [osp.H]
+    F = sum(2 * dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+    E, B = cfg.n_envs, cfg.batch
+    out = {}
+    for name, (ms, cnt) in prof.items():
+        if cnt == 0 or ms <= 0:
+            continue
+        sec = ms / 1e3
+        per = {"ms_per_step": ms / steps, "launches_per_step": cnt / steps}
+        if name in ("select", "td"):
+            n = evals[0] if name == "select" else evals[1]
+            ach = 2.0 * n / sec / 1e12
+            per.update(bound="alu", achieved=ach, peak=alu_peak, unit="Tops/s",
+                       frac=ach / alu_peak, work=f"{n / steps:.4g} Q-evals/step x 2 lane-ops",
+                       peak_src="148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)")
+        elif name in ("gemm_fwd", "gemm_bwd"):
+            rows = E + 3 * B if name == "gemm_fwd" else B
+            flops = (rows * F if name == "gemm_fwd" else B * (2 * F - 2 * dims[0] * dims[1]))
+            ach = flops * steps / sec / 1e12
+            per.update(bound="tensor", achieved=ach, peak=fp32_tc, unit="TFLOP/s",
+                       frac=ach / fp32_tc, work=f"{flops / 1e9:.4g} GFLOP/step (logical fp32)",
+                       peak_src="MEASURED_PEAKS bf16_tflops_sustained x 1/2 (tf32 ratio) x 1/3 "
+                                "(3xTF32 MMAs per fp32 product)")
+        elif name == "encode":
+            rows = E + 2 * B
+            byts = rows * (osp.W * 17 * 4 + osp.W + 8)
+            ach = byts * steps / sec / 1e9
+            per.update(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm,
+                       work=f"{byts / 1e6:.4g} MB/step")
+        elif name == "sgd":
+            n = sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1))
+            byts = n * (12 + 8 + 8)   # SGD r/w + hi/lo re-split of W and W^T
+            ach = byts * steps / sec / 1e9
+            per.update(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm,
+                       work=f"{byts / 1e6:.4g} MB/step")
+        out[name] = per
+    return out
+
+
+def dominant(rl):
+    name = max(rl, key=lambda k: rl[k]["ms_per_step"])
+    r = rl[name]
+    return {"kernel": name, "bound": r.get("bound"), "achieved": r.get("achieved"),
+            "peak": r.get("peak"), "unit": r.get("unit"), "frac": r.get("frac"),
+            "traffic": None, "peak_src": r.get("peak_src"),
+            "share_of_step": None}
 
 
 def main():

@@ -203,6 +203,9 @@ hrp_status hrp_profile_read(hrp_ctx *ctx, double *ms, int64_t *launches);
 /* Explicit Q^ evaluations (valid (l, g, sigma) scored; pruned mode: candidate assignments)
  * counted by the selection kernels since create (synchronises the stream). */
 int64_t hrp_eval_count(hrp_ctx *ctx);
+/* The same count split by kernel: out[0] = env step / inference selection, out[1] = the
+ * double-DQN target argmax of hrp_dqn_update (host int64 [2]; synchronises the stream). */
+hrp_status hrp_eval_counts(hrp_ctx *ctx, int64_t *out);
 /* Diagnostics: one tensor-core GEMM D[M][N] = A[M][K] . W[N][K]^T + bias (3xTF32, the Q-MLP
  * forward kernel) on `device` / `cuda_stream`, all pointers device; d_trace (optional,
  * uint64 [256]) receives %globaltimer stamps of CTA (0,0): [0] start, [1] setup, [2+kb] TMA

@@ -257,6 +257,7 @@ struct hrp_ctx {
   float* dsq = nullptr;
   int64_t* tmp_i64 = nullptr;         // [rows]
   unsigned long long* n_evals = nullptr;
+  unsigned* sched_ctr = nullptr;      // [2] dynamic row schedulers of the select / TD kernels
   size_t p_smem = 0;   // warp-per-state selection / TD kernels
   int sel_variant = 0; // 0 pruned argmax, 1..4 explicit enumeration with Cmax = variant
   int p_grid = 0;
@@ -518,6 +519,7 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
 hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.explicit_mode = c->explicit_mode;
   a.n_evals = c->n_evals;
+  a.ctr = c->sched_ctr;
   prof_begin(c);
   const int grid = std::min((a.M + kPWarps - 1) / kPWarps, c->p_grid);
 #define HRP_SEL(X) sel_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
@@ -659,7 +661,8 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   // argmax mode: explicit enumeration of every action needs the group tables (W <= 16)
   if (cfg->argmax_mode == 1 && hs.W > kXMaxW) return fail(HRP_ERANGE, "explicit argmax needs W <= 16");
-  c->explicit_mode = cfg->argmax_mode == 1 || (cfg->argmax_mode == 0 && hs.W <= kXMaxW);
+  if (cfg->argmax_mode == 1 && hs.T > kXS) return fail(HRP_ERANGE, "explicit argmax needs <= 128 slot types");
+  c->explicit_mode = cfg->argmax_mode == 1 || (cfg->argmax_mode == 0 && hs.W <= kXMaxW && hs.T <= kXS);
   c->gemm_mode = cfg->gemm_mode == 0 ? 2 : cfg->gemm_mode;
   if ((s = upload_tables(hs, prof, false, c->ar, c->stream, c->dt))) return s;
   // network dims and flat parameter layout (W [out][in] then b [out] per layer)
@@ -730,8 +733,10 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->bdone, R));
   CK(ar.alloc((void**)&c->dsq, R * 4));
   CK(ar.alloc((void**)&c->tmp_i64, R * 8));
-  CK(ar.alloc((void**)&c->n_evals, 8));
-  CK(cudaMemsetAsync(c->n_evals, 0, 8, c->stream));
+  CK(ar.alloc((void**)&c->n_evals, 16));  // [0] select / inference kernels, [1] TD kernel
+  CK(cudaMemsetAsync(c->n_evals, 0, 16, c->stream));
+  CK(ar.alloc((void**)&c->sched_ctr, 2 * sizeof(unsigned)));
+  CK(cudaMemsetAsync(c->sched_ctr, 0, 2 * sizeof(unsigned), c->stream));
   if (init_weights) {
     CK(cudaMemcpyAsync(c->theta, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->theta_t, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
@@ -740,7 +745,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     CK(cudaMemsetAsync(c->theta_t, 0, sizeof(float) * o, c->stream));
   }
   // selection / TD kernel launch shape (warp per state)
-  c->p_smem = pwarp_smem_bytes(hs.L, hs.T, c->explicit_mode);
+  c->p_smem = pwarp_smem_bytes(hs.L, hs.T, hs.head_width(), c->explicit_mode);
   if (c->p_smem > 227 * 1024) return fail(HRP_ERANGE, "selection tables exceed shared memory");
   {
     // the attribute is per function (process-wide): keep the largest any context needs
@@ -913,7 +918,8 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.dz = c->dz;
   t.dsq = c->dsq;
   t.astar = d_astar;
-  t.n_evals = c->n_evals;
+  t.n_evals = c->n_evals + 1;
+  t.ctr = c->sched_ctr + 1;
   prof_begin(c);
   {
     const int grid = std::min((B + kPWarps - 1) / kPWarps, c->p_grid);
@@ -1014,11 +1020,20 @@ hrp_status hrp_profile_read(hrp_ctx* c, double* ms, int64_t* count) {
 }
 
 int64_t hrp_eval_count(hrp_ctx* c) {
-  if (!c) return -1;
-  unsigned long long v = 0;
-  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return -1;
-  if (cudaMemcpy(&v, c->n_evals, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-  return (int64_t)v;
+  int64_t v[2];
+  if (hrp_eval_counts(c, v) != HRP_OK) return -1;
+  return v[0] + v[1];
+}
+
+hrp_status hrp_eval_counts(hrp_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(HRP_EINVAL, "NULL argument");
+  unsigned long long v[2] = {0, 0};
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(v, c->n_evals, sizeof(v), cudaMemcpyDeviceToHost));
+  out[0] = (int64_t)v[0];
+  out[1] = (int64_t)v[1];
+  return HRP_OK;
 }
 
 int64_t hrp_n_params(const hrp_ctx* c) { return c ? c->n_params : -1; }

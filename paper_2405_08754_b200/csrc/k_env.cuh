@@ -163,6 +163,7 @@ struct SelArgs {
   int64_t t_step;
   int N_rep;
   unsigned long long* n_evals;  // optional evaluation counter
+  unsigned* ctr;                // dynamic row scheduler (self-resetting, zero at create)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -213,6 +214,7 @@ struct TdArgs {
   float* dsq;           // [B]
   int64_t* astar;       // [B] optional
   unsigned long long* n_evals;
+  unsigned* ctr;        // dynamic row scheduler (self-resetting, zero at create)
 };
 
 // a13: theta -= lr * g ; optional target sync.

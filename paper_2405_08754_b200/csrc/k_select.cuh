@@ -38,14 +38,16 @@ namespace hrp {
 constexpr int kPWarps = 8;   // warps (states in flight) per CTA
 constexpr int kXMaxW = 16;   // explicit enumeration: window size limit
 
-__host__ __device__ constexpr int xstride(int T) { return T | 1; }  // odd: conflict-free rows
+constexpr int kXS = 128;             // explicit: cj row stride in floats (slot types T <= 128)
+constexpr int kXRows = kXMaxW + 1;   // explicit: free rows + one -inf padding row
 
 struct PWarpSmem {
   float* meanJ;   // [T] slot-type means of the job advantages
   int* top;       // pruned: [T][4] Top-C positions
   int64_t* topv;  // pruned: [T][4] their F values
-  float* cj;      // explicit: [U][xstride(T)] centred job advantages of the free positions
+  float* cj;      // explicit: [kXRows][kXS] centred job advantages of the free positions
   int* pos;       // explicit: [U] free window positions, ascending
+  float* zb;      // explicit: [H] staged head row
 };
 
 struct PTabs {
@@ -56,10 +58,11 @@ struct PTabs {
   int cstart[6];       // lay_of_c offsets per C
 };
 
-__host__ __device__ inline size_t pwarp_bytes(int T, bool x) {
+__host__ __device__ inline size_t pwarp_bytes(int T, int H, bool x) {
   size_t b = align16(sizeof(float) * T);
   if (x)
-    b += align16(sizeof(float) * kXMaxW * xstride(T)) + align16(sizeof(int) * kXMaxW);
+    b += align16(sizeof(float) * kXRows * kXS) + align16(sizeof(int) * kXMaxW) +
+         align16(sizeof(float) * H);
   else
     b += align16(sizeof(int) * T * 4) + align16(sizeof(int64_t) * T * 4);
   return b;
@@ -70,8 +73,8 @@ __host__ __device__ inline size_t ptabs_bytes(int L) {
          align16(sizeof(uint16_t) * L);
 }
 
-__host__ __device__ inline size_t pwarp_smem_bytes(int L, int T, bool x) {
-  return ptabs_bytes(L) + kPWarps * pwarp_bytes(T, x);
+__host__ __device__ inline size_t pwarp_smem_bytes(int L, int T, int H, bool x) {
+  return ptabs_bytes(L) + kPWarps * pwarp_bytes(T, H, x);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -95,16 +98,20 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
   t.stype = (uint32_t*)take(sizeof(uint32_t) * sp.L);
   t.nsl = (uint8_t*)take(sp.L);
   t.lay_of_c = (uint16_t*)take(sizeof(uint16_t) * sp.L);
-  uint8_t* wb = base + o + (threadIdx.x >> 5) * pwarp_bytes(sp.T, X > 0);
+  uint8_t* wb = base + o + (threadIdx.x >> 5) * pwarp_bytes(sp.T, sp.H, X > 0);
   w.meanJ = (float*)wb;
   wb += align16(sizeof(float) * sp.T);
   w.top = nullptr;
   w.topv = nullptr;
   w.cj = nullptr;
   w.pos = nullptr;
+  w.zb = nullptr;
   if (X > 0) {
     w.cj = (float*)wb;
-    w.pos = (int*)(wb + align16(sizeof(float) * kXMaxW * xstride(sp.T)));
+    wb += align16(sizeof(float) * kXRows * kXS);
+    w.pos = (int*)wb;
+    wb += align16(sizeof(int) * kXMaxW);
+    w.zb = (float*)wb;
   } else {
     w.top = (int*)wb;
     w.topv = (int64_t*)(wb + align16(sizeof(int) * sp.T * 4));
@@ -149,6 +156,43 @@ __device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict_
   return meanL;
 }
 
+// Copy a head row (global, H floats) into the warp's smem buffer: every lane issues all its
+// loads before any is consumed (one L2 round trip per row instead of a dependent chain).
+__device__ __forceinline__ const float* stage_row(float* dst, const float* __restrict__ src, int H) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();  // previous readers of dst are done
+  if ((H & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    const int n4 = H >> 2;
+    float4 v[4];
+    for (int i0 = 0; i0 < n4; i0 += 32 * 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * 32 + lane;
+        if (i < n4) v[u] = __ldg(s4 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * 32 + lane;
+        if (i < n4) d4[i] = v[u];
+      }
+    }
+  } else {
+    for (int i = lane; i < H; i += 32) dst[i] = __ldg(src + i);
+  }
+  __syncwarp();
+  return dst;
+}
+
+// Dynamic row scheduler: rows are handed out one at a time to warps; the counter wraps back
+// to 0 after the last warp's final (failing) fetch, so it needs no reset between launches.
+__device__ __forceinline__ int next_row(unsigned* ctr, int M, int nwarps) {
+  unsigned r = 0;
+  if ((threadIdx.x & 31) == 0) r = atomicInc(ctr, (unsigned)(M + nwarps - 1));
+  return (int)__shfl_sync(0xffffffffu, r, 0);
+}
+
 // F(cJ[j][tau]) from global z
 __device__ __forceinline__ int64_t Fj(const DevSpace& sp, const float* z, const float* meanJ, int j,
                                       int t) {
@@ -184,9 +228,9 @@ __device__ __forceinline__ float vmax(const float (&s)[N]) {
 }
 
 struct XState {
-  const float* cj;  // [U][stride]
+  const float* cj;  // [kXRows][kXS]: rows 0..U-1 = free positions, row U = -inf padding
   const int* pos;   // [U]
-  int stride, U, W;
+  int U, W;
   float thr, rm, two_delta;
   int64_t best, bidx;
   int t[4];         // this lane's layout: slot types
@@ -194,21 +238,26 @@ struct XState {
   int64_t off;      // off[l]
 };
 
-// Exact re-scoring of the permutations of subset r whose fp32 score passed the filter.
+// Exact re-scoring of the permutations of subset r whose fp32 score passed the filter: the
+// last member sits on row r[C-1] with row values m; Sp holds the C! prefix sums of the first
+// C - 1 members (perm p's last slot is perm_elem_c(C, p, C - 1)).
 template <int C>
-__device__ __forceinline__ void xverify(XState& x, const int (&r)[4], const float (&S)[fact_c(C)],
-                                        float mx) {
+__device__ __forceinline__ void xverify(XState& x, const int (&r)[4], const float (&Sp)[fact_c(C)],
+                                        const float (&m)[C]) {
   int g[4];
 #pragma unroll
   for (int i = 0; i < C; ++i) g[i] = x.pos[r[i]];
   const int64_t idx0 = x.off + rank_comb(g, C, x.W) * fact_c(C);
+  float mx = -INFINITY;
 #pragma unroll
   for (int p = 0; p < fact_c(C); ++p) {
-    if (S[p] >= x.thr) {
+    const float sp = Sp[p] + m[perm_elem_c(C, p, C - 1)];
+    mx = fmaxf(mx, sp);
+    if (sp >= x.thr) {
       int64_t q = x.base_f;
 #pragma unroll
       for (int i = 0; i < C; ++i)
-        q += fixed_point(x.cj[r[i] * x.stride + x.t[perm_elem_c(C, p, i)]]);
+        q += fixed_point(x.cj[r[i] * kXS + x.t[perm_elem_c(C, p, i)]]);
       const int64_t idx = idx0 + p;
       if (q > x.best || (q == x.best && idx < x.bidx)) {
         x.best = q;
@@ -220,8 +269,51 @@ __device__ __forceinline__ void xverify(XState& x, const int (&r)[4], const floa
   x.thr = x.rm - x.two_delta;
 }
 
-// Level K of the subset loop nest: Sp holds the P(C, K) prefix sums (Lehmer order of the
-// length-K permutation prefixes); row r_K extends them to P(C, K + 1).
+// Last level of the loop nest (the row of the last member), two rows per iteration.  The C!
+// permutation scores of a subset are Sp[p] + m[last(p)]; grouping the permutations by the
+// last member's slot c gives max_p = max_c (M[c] + m[c]) with M[c] = max of the group's
+// prefix sums, exactly in fp32 (rounding is monotone: fl(max(a, b) + c) = max(fl(a + c),
+// fl(b + c))).  So each row costs C adds and a C-way max for C! actions.  Row U is a -inf
+// padding row, so an odd trailing row needs no remainder loop.
+template <int C>
+__device__ __forceinline__ void xleaf(XState& x, int (&r)[4], const float (&Sp)[fact_c(C)],
+                                      int r_lo) {
+  float M[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) M[c] = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < fact_c(C); ++p)
+    M[perm_elem_c(C, p, C - 1)] = fmaxf(M[perm_elem_c(C, p, C - 1)], Sp[p]);
+  const float* q[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) q[k] = x.cj + r_lo * kXS + x.t[k];
+#pragma unroll 1
+  for (int rr = r_lo; rr < x.U; rr += 2) {
+    float a[C], b[C], sa[C], sb[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      a[k] = q[k][0];
+      b[k] = q[k][kXS];
+      q[k] += 2 * kXS;
+      sa[k] = M[k] + a[k];
+      sb[k] = M[k] + b[k];
+    }
+    const float va = vmax<C>(sa), vb = vmax<C>(sb);
+    if (fmaxf(va, vb) >= x.thr) {
+      if (va >= x.thr) {
+        r[C - 1] = rr;
+        xverify<C>(x, r, Sp, a);
+      }
+      if (vb >= x.thr) {
+        r[C - 1] = rr + 1;
+        xverify<C>(x, r, Sp, b);
+      }
+    }
+  }
+}
+
+// Level K < C - 1 of the subset loop nest: Sp holds the P(C, K) prefix sums (Lehmer order of
+// the length-K permutation prefixes); row r_K extends them to P(C, K + 1).
 template <int C, int K>
 __device__ __forceinline__ void xlevel(XState& x, int (&r)[4],
                                        const float (&Sp)[fact_c(C) / fact_c(C - K)], int r_lo) {
@@ -230,21 +322,17 @@ __device__ __forceinline__ void xlevel(XState& x, int (&r)[4],
 #pragma unroll 1
   for (int rr = r_lo; rr <= r_hi; ++rr) {
     r[K] = rr;
-    const float* row = x.cj + rr * x.stride;
+    const float* row = x.cj + rr * kXS;
     float m[C];
 #pragma unroll
-    for (int k = 0; k < C; ++k) m[k] = row[x.t[k]];  // C LDS (row broadcast, odd stride)
+    for (int k = 0; k < C; ++k) m[k] = row[x.t[k]];  // C LDS (one row, warp-wide)
     float S[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
       S[q] = Sp[q / (C - K)] + m[perm_elem_c(C, q * fact_c(C - K - 1), K)];
-    if constexpr (K + 1 == C) {
-      const float mx = vmax<NQ>(S);
-      if (mx >= x.thr) xverify<C>(x, r, S, mx);
-    } else {
-      xlevel<C, K + 1>(x, r, S, rr + 1);
-    }
-    if constexpr (K == 0 && C > 1) {
+    if constexpr (K + 2 == C) xleaf<C>(x, r, S, rr + 1);
+    else xlevel<C, K + 1>(x, r, S, rr + 1);
+    if constexpr (K == 0) {
       // share the running maximum across the warp (any lane's rm is a valid bound)
       x.rm = warp_maxf(x.rm);
       x.thr = x.rm - x.two_delta;
@@ -256,7 +344,8 @@ template <int C>
 __device__ __forceinline__ void xrun(XState& x, float base) {
   const float S0[1] = {base};
   int r[4] = {0, 0, 0, 0};
-  xlevel<C, 0>(x, r, S0, 0);
+  if constexpr (C == 1) xleaf<1>(x, r, S0, 0);
+  else xlevel<C, 0>(x, r, S0, 0);
 }
 
 // Greedy argmax of one state by explicit enumeration of every valid action (slot counts up to
@@ -270,7 +359,6 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
   const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
   const uint64_t freem = all & ~sched;
   const int U = __popcll(freem);
-  const int stride = xstride(T);
   __syncwarp();  // previous state's readers of cj / pos are done
   if (lane < W && ((freem >> lane) & 1ull))
     w.pos[__popcll(freem & ((1ull << lane) - 1ull))] = lane;
@@ -280,9 +368,10 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
   for (int i = lane; i < U * T; i += 32) {
     const int rr = i / T, t = i - rr * T;
     const float v = aJ[w.pos[rr] * T + t] - w.meanJ[t];
-    w.cj[rr * stride + t] = v;
+    w.cj[rr * kXS + t] = v;
     amax = fmaxf(amax, fabsf(v));
   }
+  for (int t = lane; t < T; t += 32) w.cj[U * kXS + t] = -INFINITY;  // padding row
   float lmax = 0.f;
   for (int l = lane; l < L; l += 32) lmax = fmaxf(lmax, fabsf(z[1 + l] - meanL));
   amax = warp_maxf(amax);
@@ -292,7 +381,6 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
   XState x;
   x.cj = w.cj;
   x.pos = w.pos;
-  x.stride = stride;
   x.U = U;
   x.W = W;
   x.two_delta = 2.f * ((fabsf(v) + lmax + (float)sp.cmax * amax) * 0x1p-20f + 0x1p-29f);
@@ -301,6 +389,37 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
   x.best = INT64_MIN;
   x.bidx = INT64_MAX;
   const int64_t Fv = fixed_point(v);
+  {
+    // Initial running maximum: per layout the fp32 score of one valid action (slot k takes the
+    // best still-unused free position for its type), maximised over the warp.  Its score is
+    // within delta of its exact Q^ like any fp32 evaluation, so it is a valid starting rm and
+    // lets the enumeration skip verification of all but the near-maximal actions.
+    float gmax = -FLT_MAX;
+    for (int l = lane; l < L; l += 32) {
+      const int C = tb.nsl[l];
+      if (C > U) continue;
+      const uint32_t ty = tb.stype[l];
+      float sc = v + (z[1 + l] - meanL);
+      uint32_t used = 0;
+      for (int k = 0; k < C; ++k) {
+        const int t = (ty >> (8 * k)) & 255;
+        float bv = -INFINITY;
+        int br = 0;
+        for (int rr = 0; rr < U; ++rr) {
+          const float c = w.cj[rr * kXS + t];
+          if (!((used >> rr) & 1u) && c > bv) {
+            bv = c;
+            br = rr;
+          }
+        }
+        used |= 1u << br;
+        sc += bv;
+      }
+      gmax = fmaxf(gmax, sc);
+    }
+    x.rm = warp_maxf(gmax);
+    x.thr = x.rm - x.two_delta;
+  }
   for (int C = 1; C <= CM && C <= U; ++C) {
     const int n = tb.cstart[C + 1] - tb.cstart[C];
 #pragma unroll 1
@@ -514,18 +633,18 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
 }
 
 template <int X>
-__global__ void __launch_bounds__(kPWarps * 32)
+__global__ void __launch_bounds__(kPWarps * 32, X > 0 ? 2 : 1)
 sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kPWarps + (threadIdx.x >> 5);
   const int nw = gridDim.x * kPWarps;
   const int W = sp.W;
   int64_t nevals = 0;
-  for (int row = gw; row < a.M; row += nw) {
-    const float* z = a.z + (size_t)row * sp.H;
+  for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
+    const float* zg = a.z + (size_t)row * sp.H;
+    const float* z = X > 0 ? stage_row(w.zb, zg, sp.H) : zg;
     const uint64_t sched = a.sched[row];
     const float meanL = pwarp_means(sp, z, w.meanJ);
     int64_t best, bidx;
@@ -630,30 +749,33 @@ __device__ inline float pwarp_qfloat(const DevSpace& sp, const PTabs& tb, PWarpS
 }
 
 template <int X>
-__global__ void __launch_bounds__(kPWarps * 32) td_kernel(DevSpace sp, TdArgs a) {
+__global__ void __launch_bounds__(kPWarps * 32, X > 0 ? 2 : 1) td_kernel(DevSpace sp, TdArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kPWarps + (threadIdx.x >> 5);
   const int nw = gridDim.x * kPWarps;
   const int H = sp.H, L = sp.L, T = sp.T, W = sp.W;
   int64_t nevals = 0;
-  for (int b = gw; b < a.B; b += nw) {
+  for (int b = next_row(a.ctr, a.B, nw); b < a.B; b = next_row(a.ctr, a.B, nw)) {
     const bool done = a.bdone[b] != 0;
     float y = a.br[b];
     int64_t astar = -1;
     if (!done) {
-      const float* zn = a.z_all + (size_t)(a.B + b) * H;
+      const float* zg = a.z_all + (size_t)(a.B + b) * H;
+      const float* zn = X > 0 ? stage_row(w.zb, zg, H) : zg;
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
-      const float qt = pwarp_qfloat(sp, tb, w, a.z_tgt + (size_t)b * H, astar, nullptr, nullptr,
-                                    nullptr);
+      const float* tg = a.z_tgt + (size_t)b * H;
+      const float qt = pwarp_qfloat(sp, tb, w, X > 0 ? stage_row(w.zb, tg, H) : tg, astar,
+                                    nullptr, nullptr, nullptr);
       y = a.br[b] + a.gamma * qt;
     }
     int l, g[4], tt[4];
-    const float q = pwarp_qfloat(sp, tb, w, a.z_all + (size_t)b * H, a.bact[b], &l, g, tt);
+    const float* og = a.z_all + (size_t)b * H;
+    const float q = pwarp_qfloat(sp, tb, w, X > 0 ? stage_row(w.zb, og, H) : og, a.bact[b], &l,
+                                 g, tt);
     const int C = tb.nsl[l];
     const float delta = q - y;
     if (lane == 0) {

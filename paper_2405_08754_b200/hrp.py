@@ -73,6 +73,7 @@ def lib():
             "hrp_sync": [P],
             "hrp_profile": [P, S],
             "hrp_profile_read": [P, P, P],
+            "hrp_eval_counts": [P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -255,6 +256,12 @@ def hrp_profile_read(ctx):
 
 def hrp_eval_count(ctx):
     return lib().hrp_eval_count(ctx)
+
+
+def hrp_eval_counts(ctx):
+    out = np.zeros(2, np.int64)
+    _check(lib().hrp_eval_counts(ctx, _hptr(out)))
+    return int(out[0]), int(out[1])
 
 
 def hrp_sync(ctx):
