@@ -208,6 +208,12 @@ hrp_status upload_tables(const HostSpace& hs, const hrp_profiles* prof, bool com
 struct hrp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  // side stream for the independent halves of the update (target forward beside the online
+  // forward; weight-gradient GEMMs beside the data-gradient chain); fork/join by events, so the
+  // pair is CUDA-graph capturable.  Not used while per-kernel profiling is on.
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<float*> act_t;          // target-pass hidden outputs [B][w] (concurrent scratch)
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   hrp_train_cfg cfg{};
@@ -244,10 +250,11 @@ struct hrp_ctx {
   float* z = nullptr;                 // [rows][H]
   float* zt = nullptr;                // [B][H]
   float* dz = nullptr;                // [B][H]
-  float *dh0 = nullptr, *dh1 = nullptr;  // [B][w]
+  float *dh0 = nullptr, *dh1 = nullptr;  // [B][w] (SIMT backward ping-pong)
+  std::vector<float*> dhs, dhTs;      // tensor-core backward: per hidden layer dH, dH^T
   // transposed operands of the tensor-core backward: X^T [in][B], hidden outputs^T [w][B],
   // dz^T [H][B], dh^T [w][B]
-  float *XT = nullptr, *dzT = nullptr, *dhT0 = nullptr, *dhT1 = nullptr;
+  float *XT = nullptr, *dzT = nullptr;
   std::vector<float*> actT;
   uint8_t* bwin = nullptr;            // [2B][W] or [chunk][W]
   uint64_t* bsched = nullptr;
@@ -306,6 +313,29 @@ hrp_status launch_check(hrp_ctx* c, int cls) {
   }
   return HRP_OK;
 }
+
+// Side stream waits for everything enqueued so far on the main stream.
+hrp_status fork(hrp_ctx* c) {
+  CK(cudaEventRecord(c->ev_fork, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  return HRP_OK;
+}
+// Main stream waits for everything enqueued so far on the side stream.
+hrp_status join(hrp_ctx* c) {
+  CK(cudaEventRecord(c->ev_join, c->side));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return HRP_OK;
+}
+// Run f with the context's launches redirected to the side stream.
+template <class F>
+hrp_status on_side(hrp_ctx* c, F&& f) {
+  cudaStream_t m = c->stream;
+  c->stream = c->side;
+  hrp_status s = f();
+  c->stream = m;
+  return s;
+}
+bool concurrent(const hrp_ctx* c) { return c->side != nullptr && !c->prof; }
 
 // C = epi(A . B) with the SIMT kernel; split-K (EPI_STORE) when `splitk_out` is set.
 template <bool AK, bool BKc, int EPI>
@@ -397,7 +427,8 @@ bool tc_backward(const hrp_ctx* c, int B) { return c->gemm_mode == 2 && c->tc &&
 // pass), head output z_out [M][H].  With t_rows > 0 the first t_rows rows of every hidden
 // output are also stored transposed in c->actT (operands of the weight-gradient GEMMs).
 hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out,
-                       int t_rows = 0) {
+                       int t_rows = 0, const std::vector<float*>* acts = nullptr) {
+  const std::vector<float*>& act = acts ? *acts : c->act;
   c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
   const bool target = theta == c->theta_t;
@@ -406,7 +437,7 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, fl
     const int fi = c->dims[i], fo = c->dims[i + 1];
     const float* Wm = theta + c->woff[i];
     const float* b = Wm + (int64_t)fi * fo;
-    float* out = (i == nl - 1) ? z_out : c->act[i];
+    float* out = (i == nl - 1) ? z_out : act[i];
     float* outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : nullptr;
     hrp_status s;
     if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(M, fo, fi)) {
@@ -432,33 +463,38 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
   c->gemm_cls = HRP_K_GEMM_BWD;
   const int nl = (int)c->dims.size() - 1;
   const int H = c->dims[nl];
+  const bool conc = concurrent(c);
   hrp_status s;
   if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, H, c->dz, c->dzT))) return s;
+  if (conc && (s = fork(c))) return s;
   const float* dY = c->dz;
   const float* dYT = c->dzT;
-  float* bufs[2] = {c->dh0, c->dh1};
-  float* bufsT[2] = {c->dhT0, c->dhT1};
-  int cur = 0;
   for (int i = nl - 1; i >= 0; --i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
     const float* HinT = (i == 0) ? c->XT : c->actT[i - 1];
     const float* Hin = (i == 0) ? c->X : c->act[i - 1];
     float* gW = c->grad + c->woff[i];
     float* gb = gW + (int64_t)fi * fo;
-    // dW [fo][fi] = dY^T . Hin = (dYT [fo][B]) . (HinT [fi][B])^T
-    prof_begin(c);
-    s = tc_gemm_wgrad(c->tc, c->stream, fo, fi, B, dYT, HinT, c->ws_splitk, c->ws_splitk_elems, gW);
-    if (s) return fail(s, tc_gemm_error());
-    c->launches += tc_gemm_launches(c->tc) - 1;
-    if ((s = launch_check(c, HRP_K_GEMM_BWD))) return s;
-    prof_begin(c);
-    s = tc_rowsum(c->tc, c->stream, fo, B, dYT, gb);
-    if (s) return fail(s, tc_gemm_error());
-    c->launches += tc_gemm_launches(c->tc) - 1;
-    if ((s = launch_check(c, HRP_K_GEMM_BWD))) return s;
+    // weight and bias gradients (side stream): dW [fo][fi] = dY^T . Hin = dYT . HinT^T
+    auto wgrad = [&]() -> hrp_status {
+      prof_begin(c);
+      hrp_status t = tc_gemm_wgrad(c->tc, c->stream, fo, fi, B, dYT, HinT, c->ws_splitk,
+                                   c->ws_splitk_elems, gW);
+      if (t) return fail(t, tc_gemm_error());
+      c->launches += tc_gemm_launches(c->tc) - 1;
+      if ((t = launch_check(c, HRP_K_GEMM_BWD))) return t;
+      prof_begin(c);
+      t = tc_rowsum(c->tc, c->stream, fo, B, dYT, gb);
+      if (t) return fail(t, tc_gemm_error());
+      c->launches += tc_gemm_launches(c->tc) - 1;
+      return launch_check(c, HRP_K_GEMM_BWD);
+    };
+    s = conc ? on_side(c, wgrad) : wgrad();
+    if (s) return s;
     if (i > 0) {
-      float* dH = bufs[cur];
-      float* dHT = bufsT[cur];
+      // data gradient (main stream): dH = (dY . W) * ReLU'(Hin), and its transpose
+      float* dH = c->dhs[i - 1];
+      float* dHT = c->dhTs[i - 1];
       if (tc_gemm_supported(B, fi, fo)) {
         const float* hT = c->wsplitT + c->soff[i];
         s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->sstride,
@@ -469,11 +505,12 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
         if (!s) s = transpose(c, HRP_K_GEMM_BWD, B, fi, fi, dH, dHT);
       }
       if (s) return s;
+      if (conc && (s = fork(c))) return s;
       dY = dH;
       dYT = dHT;
-      cur ^= 1;
     }
   }
+  if (conc && (s = join(c))) return s;
   return HRP_OK;
 }
 
@@ -521,7 +558,8 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.n_evals = c->n_evals;
   a.ctr = c->sched_ctr;
   prof_begin(c);
-  const int grid = std::min((a.M + kPWarps - 1) / kPWarps, c->p_grid);
+  const int rpc = sel_rows_per_cta(c->explicit_mode);
+  const int grid = std::min((a.M + rpc - 1) / rpc, c->p_grid);
 #define HRP_SEL(X) sel_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
   HRP_VARIANT(c->sel_variant, HRP_SEL);
 #undef HRP_SEL
@@ -615,6 +653,12 @@ hrp_status hrp_env_destroy(hrp_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->tc) tc_gemm_destroy(c->tc);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   c->ar.release();
   delete c;
   return HRP_OK;
@@ -719,13 +763,20 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->dh1, sizeof(float) * (size_t)B * wd));
   CK(ar.alloc((void**)&c->XT, sizeof(float) * (size_t)B * in));
   CK(ar.alloc((void**)&c->dzT, sizeof(float) * (size_t)B * H));
-  CK(ar.alloc((void**)&c->dhT0, sizeof(float) * (size_t)B * wd));
-  CK(ar.alloc((void**)&c->dhT1, sizeof(float) * (size_t)B * wd));
   for (int i = 0; i < cfg->hidden_layers; ++i) {
-    float* p;
+    float *p, *q, *u, *v;
     CK(ar.alloc((void**)&p, sizeof(float) * (size_t)B * wd));
+    CK(ar.alloc((void**)&q, sizeof(float) * (size_t)B * wd));
+    CK(ar.alloc((void**)&u, sizeof(float) * (size_t)B * wd));
+    CK(ar.alloc((void**)&v, sizeof(float) * (size_t)B * wd));
     c->actT.push_back(p);
+    c->act_t.push_back(q);
+    c->dhs.push_back(u);
+    c->dhTs.push_back(v);
   }
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(ar.alloc((void**)&c->bwin, R * W));
   CK(ar.alloc((void**)&c->bsched, R * 8));
   CK(ar.alloc((void**)&c->bact, R * 8));
@@ -892,17 +943,21 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
   const bool tcb = tc_backward(c, B);
   if (tcb && (s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->dims[0], c->X, c->XT))) return s;
-  // online net on [s; s'] (activations of the s rows kept for backward), target on s'
+  // online net on [s; s'] (activations of the s rows kept for backward) on the main stream,
+  // target net on s' beside it (its own activation scratch)
+  const bool conc = concurrent(c);
+  if (conc && (s = fork(c))) return s;
+  auto target_pass = [&]() {
+    return mlp_forward(c, c->theta_t, c->X + (size_t)B * c->dims[0], B, c->zt, 0, &c->act_t);
+  };
+  if (conc) {
+    if ((s = on_side(c, target_pass))) return s;
+  }
   if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, tcb ? B : 0))) return s;
-  // target forward reuses act buffers rows [B,2B) scratch: run on X rows [B,2B) into zt
-  {
-    // hidden activations of the target pass must not clobber rows [0,B) kept for backward:
-    // the act buffers hold 2B rows; point the target pass at rows [B, 2B).
-    std::vector<float*> saved = c->act;
-    for (auto& p : c->act) p += (size_t)B * c->cfg.hidden_width;
-    s = mlp_forward(c, c->theta_t, c->X + (size_t)B * c->dims[0], B, c->zt);
-    c->act = saved;
-    if (s) return s;
+  if (conc) {
+    if ((s = join(c))) return s;
+  } else if ((s = target_pass())) {
+    return s;
   }
   TdArgs t{};
   t.B = B;
@@ -922,7 +977,8 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.ctr = c->sched_ctr + 1;
   prof_begin(c);
   {
-    const int grid = std::min((B + kPWarps - 1) / kPWarps, c->p_grid);
+    const int rpc = sel_rows_per_cta(c->explicit_mode);
+    const int grid = std::min((B + rpc - 1) / rpc, c->p_grid);
 #define HRP_TD(X) td_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, t)
     HRP_VARIANT(c->sel_variant, HRP_TD);
 #undef HRP_TD

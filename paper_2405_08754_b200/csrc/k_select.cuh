@@ -38,16 +38,16 @@ namespace hrp {
 constexpr int kPWarps = 8;   // warps (states in flight) per CTA
 constexpr int kXMaxW = 16;   // explicit enumeration: window size limit
 
-constexpr int kXS = 128;             // explicit: cj row stride in floats (slot types T <= 128)
-constexpr int kXRows = kXMaxW + 1;   // explicit: free rows + one -inf padding row
+constexpr int kXS = 128;             // explicit: slot types T <= 128
+constexpr int kXRows = kXMaxW + 1;   // explicit: free rows + one -inf padding row (odd: the
+                                     // type-major cj stride, conflict-free across types)
 
 struct PWarpSmem {
   float* meanJ;   // [T] slot-type means of the job advantages
   int* top;       // pruned: [T][4] Top-C positions
   int64_t* topv;  // pruned: [T][4] their F values
-  float* cj;      // explicit: [kXRows][kXS] centred job advantages of the free positions
+  float* cj;      // explicit: [T][kXRows] centred job advantages of the free positions (type-major)
   int* pos;       // explicit: [U] free window positions, ascending
-  float* zb;      // explicit: [H] staged head row
 };
 
 struct PTabs {
@@ -61,8 +61,7 @@ struct PTabs {
 __host__ __device__ inline size_t pwarp_bytes(int T, int H, bool x) {
   size_t b = align16(sizeof(float) * T);
   if (x)
-    b += align16(sizeof(float) * kXRows * kXS) + align16(sizeof(int) * kXMaxW) +
-         align16(sizeof(float) * H);
+    b += align16(sizeof(float) * kXRows * T) + align16(sizeof(int) * kXMaxW);
   else
     b += align16(sizeof(int) * T * 4) + align16(sizeof(int64_t) * T * 4);
   return b;
@@ -76,6 +75,9 @@ __host__ __device__ inline size_t ptabs_bytes(int L) {
 __host__ __device__ inline size_t pwarp_smem_bytes(int L, int T, int H, bool x) {
   return ptabs_bytes(L) + kPWarps * pwarp_bytes(T, H, x);
 }
+
+// rows (states) one CTA owns at a time
+__host__ __device__ constexpr int sel_rows_per_cta(bool) { return kPWarps; }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -105,13 +107,10 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
   w.topv = nullptr;
   w.cj = nullptr;
   w.pos = nullptr;
-  w.zb = nullptr;
   if (X > 0) {
     w.cj = (float*)wb;
-    wb += align16(sizeof(float) * kXRows * kXS);
+    wb += align16(sizeof(float) * kXRows * sp.T);
     w.pos = (int*)wb;
-    wb += align16(sizeof(int) * kXMaxW);
-    w.zb = (float*)wb;
   } else {
     w.top = (int*)wb;
     w.topv = (int64_t*)(wb + align16(sizeof(int) * sp.T * 4));
@@ -154,35 +153,6 @@ __device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict_
   }
   __syncwarp();
   return meanL;
-}
-
-// Copy a head row (global, H floats) into the warp's smem buffer: every lane issues all its
-// loads before any is consumed (one L2 round trip per row instead of a dependent chain).
-__device__ __forceinline__ const float* stage_row(float* dst, const float* __restrict__ src, int H) {
-  const int lane = threadIdx.x & 31;
-  __syncwarp();  // previous readers of dst are done
-  if ((H & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    const int n4 = H >> 2;
-    float4 v[4];
-    for (int i0 = 0; i0 < n4; i0 += 32 * 4) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * 32 + lane;
-        if (i < n4) v[u] = __ldg(s4 + i);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * 32 + lane;
-        if (i < n4) d4[i] = v[u];
-      }
-    }
-  } else {
-    for (int i = lane; i < H; i += 32) dst[i] = __ldg(src + i);
-  }
-  __syncwarp();
-  return dst;
 }
 
 // Dynamic row scheduler: rows are handed out one at a time to warps; the counter wraps back
@@ -228,7 +198,7 @@ __device__ __forceinline__ float vmax(const float (&s)[N]) {
 }
 
 struct XState {
-  const float* cj;  // [kXRows][kXS]: rows 0..U-1 = free positions, row U = -inf padding
+  const float* cj;  // [T][kXRows]: rows 0..U-1 = free positions, row U = -inf padding
   const int* pos;   // [U]
   int U, W;
   float thr, rm, two_delta;
@@ -257,7 +227,7 @@ __device__ __forceinline__ void xverify(XState& x, const int (&r)[4], const floa
       int64_t q = x.base_f;
 #pragma unroll
       for (int i = 0; i < C; ++i)
-        q += fixed_point(x.cj[r[i] * kXS + x.t[perm_elem_c(C, p, i)]]);
+        q += fixed_point(x.cj[x.t[perm_elem_c(C, p, i)] * kXRows + r[i]]);
       const int64_t idx = idx0 + p;
       if (q > x.best || (q == x.best && idx < x.bidx)) {
         x.best = q;
@@ -286,15 +256,15 @@ __device__ __forceinline__ void xleaf(XState& x, int (&r)[4], const float (&Sp)[
     M[perm_elem_c(C, p, C - 1)] = fmaxf(M[perm_elem_c(C, p, C - 1)], Sp[p]);
   const float* q[C];
 #pragma unroll
-  for (int k = 0; k < C; ++k) q[k] = x.cj + r_lo * kXS + x.t[k];
+  for (int k = 0; k < C; ++k) q[k] = x.cj + x.t[k] * kXRows + r_lo;
 #pragma unroll 1
   for (int rr = r_lo; rr < x.U; rr += 2) {
     float a[C], b[C], sa[C], sb[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       a[k] = q[k][0];
-      b[k] = q[k][kXS];
-      q[k] += 2 * kXS;
+      b[k] = q[k][1];
+      q[k] += 2;
       sa[k] = M[k] + a[k];
       sb[k] = M[k] + b[k];
     }
@@ -322,10 +292,9 @@ __device__ __forceinline__ void xlevel(XState& x, int (&r)[4],
 #pragma unroll 1
   for (int rr = r_lo; rr <= r_hi; ++rr) {
     r[K] = rr;
-    const float* row = x.cj + rr * kXS;
     float m[C];
 #pragma unroll
-    for (int k = 0; k < C; ++k) m[k] = row[x.t[k]];  // C LDS (one row, warp-wide)
+    for (int k = 0; k < C; ++k) m[k] = x.cj[x.t[k] * kXRows + rr];  // C LDS (one row, warp-wide)
     float S[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -368,10 +337,10 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
   for (int i = lane; i < U * T; i += 32) {
     const int rr = i / T, t = i - rr * T;
     const float v = aJ[w.pos[rr] * T + t] - w.meanJ[t];
-    w.cj[rr * kXS + t] = v;
+    w.cj[t * kXRows + rr] = v;
     amax = fmaxf(amax, fabsf(v));
   }
-  for (int t = lane; t < T; t += 32) w.cj[U * kXS + t] = -INFINITY;  // padding row
+  for (int t = lane; t < T; t += 32) w.cj[t * kXRows + U] = -INFINITY;  // padding row
   float lmax = 0.f;
   for (int l = lane; l < L; l += 32) lmax = fmaxf(lmax, fabsf(z[1 + l] - meanL));
   amax = warp_maxf(amax);
@@ -406,7 +375,7 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
         float bv = -INFINITY;
         int br = 0;
         for (int rr = 0; rr < U; ++rr) {
-          const float c = w.cj[rr * kXS + t];
+          const float c = w.cj[t * kXRows + rr];
           if (!((used >> rr) & 1u) && c > bv) {
             bv = c;
             br = rr;
@@ -633,7 +602,7 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
 }
 
 template <int X>
-__global__ void __launch_bounds__(kPWarps * 32, X > 0 ? 2 : 1)
+__global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4))
 sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
@@ -644,7 +613,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   int64_t nevals = 0;
   for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
     const float* zg = a.z + (size_t)row * sp.H;
-    const float* z = X > 0 ? stage_row(w.zb, zg, sp.H) : zg;
+    const float* z = zg;
     const uint64_t sched = a.sched[row];
     const float meanL = pwarp_means(sp, z, w.meanJ);
     int64_t best, bidx;
@@ -749,7 +718,7 @@ __device__ inline float pwarp_qfloat(const DevSpace& sp, const PTabs& tb, PWarpS
 }
 
 template <int X>
-__global__ void __launch_bounds__(kPWarps * 32, X > 0 ? 2 : 1) td_kernel(DevSpace sp, TdArgs a) {
+__global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) td_kernel(DevSpace sp, TdArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
@@ -763,18 +732,18 @@ __global__ void __launch_bounds__(kPWarps * 32, X > 0 ? 2 : 1) td_kernel(DevSpac
     int64_t astar = -1;
     if (!done) {
       const float* zg = a.z_all + (size_t)(a.B + b) * H;
-      const float* zn = X > 0 ? stage_row(w.zb, zg, H) : zg;
+      const float* zn = zg;
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
       const float* tg = a.z_tgt + (size_t)b * H;
-      const float qt = pwarp_qfloat(sp, tb, w, X > 0 ? stage_row(w.zb, tg, H) : tg, astar,
+      const float qt = pwarp_qfloat(sp, tb, w, tg, astar,
                                     nullptr, nullptr, nullptr);
       y = a.br[b] + a.gamma * qt;
     }
     int l, g[4], tt[4];
     const float* og = a.z_all + (size_t)b * H;
-    const float q = pwarp_qfloat(sp, tb, w, X > 0 ? stage_row(w.zb, og, H) : og, a.bact[b], &l,
+    const float q = pwarp_qfloat(sp, tb, w, og, a.bact[b], &l,
                                  g, tt);
     const int C = tb.nsl[l];
     const float delta = q - y;
