@@ -209,10 +209,12 @@ hrp_status hrp_eval_counts(hrp_ctx *ctx, int64_t *out);
 /* Diagnostics: one tensor-core GEMM D[M][N] = A[M][K] . W[N][K]^T + bias (3xTF32, the Q-MLP
  * forward kernel) on `device` / `cuda_stream`, all pointers device; d_trace (optional,
  * uint64 [256]) receives %globaltimer stamps of CTA (0,0): [0] start, [1] setup, [2+kb] TMA
- * issue, [66+kb] split done, [130+kb] MMA issued, [194] accumulator ready, [195] end. */
+ * issue, [130+kb] MMA issued, [194] accumulator ready, [195] end.  With reps > 0 and ms_out,
+ * *ms_out = the average device time of `reps` further back-to-back GEMM launches (operands
+ * already split).  force_bn: output tile width 64 / 128 / 256, 0 = the library's choice. */
 hrp_status hrp_diag_gemm(int device, void *cuda_stream, int M, int N, int K, const float *d_A,
                          const float *d_W, const float *d_bias, float *d_D,
-                         uint64_t *d_trace);
+                         uint64_t *d_trace, int reps, int force_bn, float *ms_out);
 /* Block until the context's stream is idle; returns any pending CUDA/NCCL error. */
 hrp_status hrp_sync(hrp_ctx *ctx);
 const char *hrp_last_error(void);

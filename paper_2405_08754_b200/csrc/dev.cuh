@@ -43,6 +43,14 @@ __device__ __forceinline__ uint64_t slot_pack_sm(uint32_t s) { return s & 0xffff
 static __device__ int64_t c_binom[65][5];
 static __device__ int64_t c_fact[5];
 
+// tf32 round-to-nearest (ties away) of an fp32 value: the hi part of a 3xTF32 operand split;
+// lo = x - hi is exact in fp32.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 __device__ __forceinline__ int64_t fixed_point(float x) {
   // F(x) = round-half-even(x * 2^32): the power-of-two scale is exact in fp32 (no overflow for
   // |x| < 2^95), and cvt.rni.s64.f32 rounds the exact product half-to-even.

@@ -5,21 +5,24 @@
 //   D ~= A_hi B_hi + A_hi B_lo + A_lo B_hi  (relative error ~2^-21 per product, fp32 accumulate
 //   in TMEM) -- the precision the oracle parity (1e-4, BASELINE north star) needs.
 //
-// Uses (all operands K-major, i.e. row-major with the reduction dimension contiguous):
-//   forward        A = activations [rows][in],  B = W [out][in] (pre-split hi/lo)
-//   backward-data  A = dY [rows][out],          B = W^T [in][out] (pre-split hi/lo)
-//   weight-grad    A = dY^T [out][rows],        B = H^T [in][rows] (split in smem), split-K
+// Every operand arrives pre-split as two planes (hi, lo): the producer of an activation (the
+// previous GEMM's epilogue, the encoder, the TD kernel) writes it split once, so the main loop
+// is TMA -> MMA with no conversion stage.  Uses (all operands K-major, i.e. row-major with the
+// reduction dimension contiguous):
+//   forward        A = activations [rows][in],  B = W [out][in]
+//   backward-data  A = dY [rows][out],          B = W^T [in][out]
+//   weight-grad    A = dY^T [out][rows],        B = H^T [in][rows], split-K
 //
 // Structure (one 128 x BN output tile per CTA, 256 threads):
-//   warp 0      TMA producer: A tile (raw fp32, 128 x 32, SWIZZLE_128B) + B tiles per stage,
-//               mbarrier expect_tx
+//   warp 0      TMA producer: A hi/lo tiles (128 x 32 fp32, SWIZZLE_128B) + B hi/lo tiles per
+//               stage, mbarrier expect_tx
 //   warp 1      MMA issuer (one lane): 3 x tcgen05.mma.kind::tf32 per K=8 step,
 //               tcgen05.commit -> stage empty / accumulator full
 //   warp 2      TMEM allocator (BN columns)
-//   warps 4-7   split the raw tiles in shared memory (hi in place, lo beside it;
-//               fence.proxy.async), then the epilogue: tcgen05.ld 32x32b -> per-warp 32x33 smem
-//               transpose -> bias / ReLU / ReLU-mask -> coalesced stores of D and (optionally)
-//               of D^T for the first t_rows rows (the backward pass's transposed operands).
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> per-warp 32x33 smem transpose -> bias / ReLU /
+//               ReLU-mask -> coalesced stores of D (raw, or split into hi/lo planes for the
+//               next GEMM) and optionally of D^T for the first t_rows rows (the backward
+//               pass's transposed operands, also split).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -136,14 +139,17 @@ struct TcSmem {
 
 struct TcArgs {
   int M, N, K;
+  int lda, ldb;            // row strides (elements, multiples of 4) of the A / B planes
   int boxA, boxB;
   int kc;                  // K range per blockIdx.z (multiple of BK)
   const float* bias;
   const float* aux;        // ReLU mask source [M][ldaux]
   int ldaux;
   float* D;                // [M][ldd]; split-K: + blockIdx.z * M * ldd
+  float* Dlo;              // optional: D is written split, hi -> D, lo -> Dlo
   int ldd;
-  float* DT;               // optional D^T [N][ldt] for rows < t_rows
+  float* DT;               // optional D^T [N][ldt] for rows < t_rows (split: hi -> DT, lo -> DTlo)
+  float* DTlo;
   int ldt, t_rows;
   unsigned long long* trace;  // diagnostics: per-event timestamps of CTA (0,0,0), or null
 };
@@ -153,30 +159,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// trace slots: [0] start, [1] setup done, [2+kb] TMA issued, [66+kb] split done,
-// [130+kb] MMA issued, [194] acc ready, [195] epilogue done
+// trace slots: [0] start, [1] setup done, [2+kb] TMA issued, [130+kb] MMA issued,
+// [194] acc ready, [195] epilogue done
 #define TRACE(slot)                                                                         \
   do {                                                                                      \
     if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) a.trace[slot] = gtimer(); \
   } while (0)
 
-__device__ __forceinline__ void split_tile(uint8_t* hi, uint8_t* lo, int bytes, int t) {
-  float4* h4 = reinterpret_cast<float4*>(hi);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-  for (int idx = t; idx < bytes / 16; idx += 128) {
-    const float4 x = h4[idx];
-    const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-    h4[idx] = h;
-    l4[idx] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+// Store v at p (raw), or split into planes: hi -> p, lo -> plo.
+__device__ __forceinline__ void store_split(float* p, float* plo, float v) {
+  if (plo) {
+    const float h = tf32_rna(v);
+    *p = h;
+    *plo = v - h;
+  } else {
+    *p = v;
   }
 }
 
-// SPLITB: B arrives raw through mapB0 and is split in shared memory like A; otherwise mapB0 /
-// mapB1 carry the pre-split hi / lo planes.
-template <int BN, int STAGES, int EPI, bool SPLITB>
+// mapA0/mapA1: A hi/lo planes; mapB0/mapB1: B hi/lo planes.
+template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreadsTc, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB0,
-               const __grid_constant__ CUtensorMap mapB1, const TcArgs a) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+               const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
+               const TcArgs a) {
   using S = TcSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -186,10 +192,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   auto b_lo = [&](int s) { return smem + s * S::STAGE_BYTES + 2 * S::A_BYTES + S::B_BYTES; };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * S::STAGE_BYTES);
   uint64_t* full_bar = bars;               // TMA landed
-  uint64_t* conv_bar = bars + STAGES;      // split done
-  uint64_t* empty_bar = bars + 2 * STAGES; // MMA finished reading the stage
-  uint64_t* acc_bar = bars + 3 * STAGES;   // accumulator complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  uint64_t* empty_bar = bars + STAGES;     // MMA finished reading the stage
+  uint64_t* acc_bar = bars + 2 * STAGES;   // accumulator complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -199,13 +204,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   if (threadIdx.x == 0) TRACE(0);
 
   if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA0)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA1)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB0)) : "memory");
-    if (!SPLITB)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB1)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&conv_bar[s], 128);
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(acc_bar, 1);
@@ -225,15 +229,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(a.boxA + (SPLITB ? 1 : 2) * a.boxB) * BK * 4;
+      const uint32_t bytes = (uint32_t)(2 * (a.boxA + a.boxB)) * BK * 4;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty_bar[s], ((kb / STAGES) - 1) & 1);
         mbar_expect_tx(&full_bar[s], bytes);
         const int kk = kbeg + kb * BK;
-        tma_load_2d(a_hi(s), &mapA, &full_bar[s], kk, m0);
+        tma_load_2d(a_hi(s), &mapA0, &full_bar[s], kk, m0);
+        tma_load_2d(a_lo(s), &mapA1, &full_bar[s], kk, m0);
         tma_load_2d(b_hi(s), &mapB0, &full_bar[s], kk, n0);
-        if (!SPLITB) tma_load_2d(b_lo(s), &mapB1, &full_bar[s], kk, n0);
+        tma_load_2d(b_lo(s), &mapB1, &full_bar[s], kk, n0);
         if (kb < 64) TRACE(2 + kb);
       }
     }
@@ -242,7 +247,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
       constexpr uint32_t idesc = idesc_tf32<BN>();
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
-        mbar_wait(&conv_bar[s], (kb / STAGES) & 1);
+        mbar_wait(&full_bar[s], (kb / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint64_t dah = smem_desc(a_hi(s)), dal = smem_desc(a_lo(s));
         const uint64_t dbh = smem_desc(b_hi(s)), dbl = smem_desc(b_lo(s));
@@ -259,48 +264,47 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
       }
       mma_commit(acc_bar);
     }
-  } else if (warp >= 4) {
-    const int t = threadIdx.x - 128;  // 0..127
-    if (EPI == TC_EPI_RELU_MASK) {
-      // warm L2 with this tile's ReLU-mask rows now, so the epilogue's reads do not stall
-      const int row = m0 + t;
-      if (row < a.M)
-        for (int cb = n0; cb < min(a.N, n0 + BN); cb += 32)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.aux + (size_t)row * a.ldaux + cb));
-    }
-    // ---- split raw tiles: hi = rna_tf32(x) in place, lo = x - hi ----
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full_bar[s], (kb / STAGES) & 1);
-      split_tile(a_hi(s), a_lo(s), S::A_BYTES, t);
-      if (SPLITB) split_tile(b_hi(s), b_lo(s), S::B_BYTES, t);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&conv_bar[s]);
-      if (t == 0 && kb < 64) TRACE(66 + kb);
-    }
-    // ---- epilogue: TMEM -> registers -> smem (per-warp 32 x 33) -> coalesced D (and D^T) ----
-    const int wq = warp & 3;                 // TMEM lane quarter of this warp = its 32 rows
+  } else if (warp >= 4 && EPI == TC_EPI_RELU_MASK) {
+    // warm L2 with this tile's ReLU-mask rows now, so the epilogue's reads do not stall
+    const int row = m0 + threadIdx.x - 128;
+    if (row < a.M)
+      for (int cb = n0; cb < min(a.N, n0 + BN); cb += 32)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.aux + (size_t)row * a.ldaux + cb));
+  }
+  __syncwarp();
+  {
+    // ---- epilogue, all 8 warps: warp w reads TMEM lane quarter (w & 3) = rows 32(w & 3).. and
+    // every other 32-column chunk starting at chunk (w >> 2); TMEM -> registers -> smem (per-warp
+    // 32 x 33) -> coalesced D (and D^T) ----
+    constexpr int NCH = BN / 32;
+    const int wq = warp & 3, wh = warp >> 2;
     const int rbase = m0 + wq * 32;
-    // bias of every column chunk this lane will write, loaded before the accumulator is ready
-    float bias_r[BN / 32];
+    float bias_r[(NCH + 1) / 2];
 #pragma unroll
-    for (int q = 0; q < BN / 32; ++q) {
-      const int col = n0 + q * 32 + lane;
-      bias_r[q] = ((EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) && col < a.N) ? a.bias[col] : 0.f;
+    for (int u = 0; u < (NCH + 1) / 2; ++u) {
+      const int col = n0 + (2 * u + wh) * 32 + lane;
+      bias_r[u] = ((EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) && 2 * u + wh < NCH && col < a.N)
+                      ? a.bias[col] : 0.f;
     }
     mbar_wait(acc_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (t == 0) TRACE(194);
+    if (threadIdx.x == 128) TRACE(194);
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    float* stg = reinterpret_cast<float*>(smem) + wq * (32 * 33);  // stage buffers are idle now
+    // the stage buffers are idle now: per-warp 32 x 33 transpose tile
+    float* stg = reinterpret_cast<float*>(smem) + warp * (32 * 33);
     float* Dz = a.D + (size_t)blockIdx.z * a.M * a.ldd;
+    const bool dsplit = a.Dlo != nullptr, tsplit = a.DTlo != nullptr;
+    const ptrdiff_t dlo = dsplit ? a.Dlo - a.D : 0;
+    const ptrdiff_t dtlo = tsplit ? a.DTlo - a.DT : 0;
 #pragma unroll
-    for (int q = 0; q < BN / 32; ++q) {
+    for (int u = 0; u < (NCH + 1) / 2; ++u) {
+      const int q = 2 * u + wh;
+      if (q >= NCH) break;                     // warp-uniform
       const int c = q * 32;
+      if (n0 + c >= a.N) break;                // warp-uniform
       uint32_t v[32];
       TMEM_LD32(trow + c, v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (n0 + c >= a.N) break;                // warp-uniform
       const int col = n0 + c + lane;
       float mk[32];
       if (EPI == TC_EPI_RELU_MASK) {           // all 32 mask loads in flight at once
@@ -313,15 +317,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 #pragma unroll
       for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = __uint_as_float(v[j]);
       __syncwarp();
-#pragma unroll
+#pragma unroll 8
       for (int r = 0; r < 32; ++r) {
         const int row = rbase + r;
         if (row < a.M && col < a.N) {
           float x = stg[r * 33 + lane];
-          if (EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) x += bias_r[q];
+          if (EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) x += bias_r[u];
           if (EPI == TC_EPI_BIAS_RELU) x = fmaxf(x, 0.f);
           if (EPI == TC_EPI_RELU_MASK) x = mk[r] > 0.f ? x : 0.f;
-          Dz[(size_t)row * a.ldd + col] = x;
+          float* dp = Dz + (size_t)row * a.ldd + col;
+          store_split(dp, dsplit ? dp + dlo : nullptr, x);
           stg[r * 33 + lane] = x;
         }
       }
@@ -331,7 +336,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
 #pragma unroll 4
         for (int r = 0; r < 32; ++r) {
           const int cc = n0 + c + r;
-          if (cc < a.N && row < a.t_rows && row < a.M) a.DT[(size_t)cc * a.ldt + row] = stg[lane * 33 + r];
+          if (cc < a.N && row < a.t_rows && row < a.M) {
+            float* tp = a.DT + (size_t)cc * a.ldt + row;
+            store_split(tp, tsplit ? tp + dtlo : nullptr, stg[lane * 33 + r]);
+          }
         }
       }
       __syncwarp();
@@ -345,19 +353,22 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__
   }
 }
 
-// hi/lo split of a weight matrix W [rows][cols] (and optionally its transpose).
-__global__ void split_kernel(int64_t n, const float* __restrict__ w, float* __restrict__ hi,
-                             float* __restrict__ lo) {
+// hi/lo split of a matrix W [rows][cols] into planes with row stride ld (and optionally of its
+// transpose).
+__global__ void split_kernel(int rows, int cols, int ld, const float* __restrict__ w,
+                             float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t n = (int64_t)rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
     const float x = w[i];
     const float h = tf32_rna(x);
-    hi[i] = h;
-    lo[i] = x - h;
+    hi[r * ld + c] = h;
+    lo[r * ld + c] = x - h;
   }
 }
 
-__global__ void split_t_kernel(int rows, int cols, const float* __restrict__ w,
+__global__ void split_t_kernel(int rows, int cols, int ldt, const float* __restrict__ w,
                                float* __restrict__ hi, float* __restrict__ lo) {
   __shared__ float tile[32][33];
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
@@ -371,16 +382,20 @@ __global__ void split_t_kernel(int rows, int cols, const float* __restrict__ w,
     if (c < cols && r < rows) {
       const float x = tile[threadIdx.x][i];
       const float h = tf32_rna(x);
-      hi[(size_t)c * rows + r] = h;
-      lo[(size_t)c * rows + r] = x - h;
+      hi[(size_t)c * ldt + r] = h;
+      lo[(size_t)c * ldt + r] = x - h;
     }
   }
 }
 
-// dst[c][r] = src[r][c]
-__global__ void transpose_kernel(int rows, int cols, int ld_src, const float* __restrict__ src,
-                                 int ld_dst, float* __restrict__ dst) {
+// dst[c][r] = src[r][c] for both planes (blockIdx.z = plane).  Transposing the hi and lo planes
+// separately equals splitting the transposed value (the split is elementwise).
+__global__ void transpose_kernel(int rows, int cols, int ld_src, const float* __restrict__ src0,
+                                 const float* __restrict__ src1, int ld_dst,
+                                 float* __restrict__ dst0, float* __restrict__ dst1) {
   __shared__ float tile[32][33];
+  const float* src = blockIdx.z ? src1 : src0;
+  float* dst = blockIdx.z ? dst1 : dst0;
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
@@ -393,22 +408,24 @@ __global__ void transpose_kernel(int rows, int cols, int ld_src, const float* __
   }
 }
 
-// out[r] = sum_c src[r][c], one warp per row, fixed (deterministic) order.
-__global__ void rowsum_kernel(int rows, int cols, const float* __restrict__ src,
-                              float* __restrict__ out) {
+// out[r] = sum_c (hi[r][c] + lo[r][c]), one warp per row, fixed (deterministic) order.
+__global__ void rowsum_kernel(int rows, int cols, const float* __restrict__ hi,
+                              const float* __restrict__ lo, float* __restrict__ out) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= rows) return;
-  const float* p = src + (size_t)w * cols;
+  const float* p = hi + (size_t)w * cols;
+  const float* q = lo + (size_t)w * cols;
   float s = 0.f;
   if ((cols & 3) == 0) {
     const float4* p4 = reinterpret_cast<const float4*>(p);
+    const float4* q4 = reinterpret_cast<const float4*>(q);
     for (int c = lane; c < cols / 4; c += 32) {
-      const float4 v = p4[c];
-      s += (v.x + v.y) + (v.z + v.w);
+      const float4 u = p4[c], v = q4[c];
+      s += ((u.x + v.x) + (u.y + v.y)) + ((u.z + v.z) + (u.w + v.w));
     }
   } else {
-    for (int c = lane; c < cols; c += 32) s += p[c];
+    for (int c = lane; c < cols; c += 32) s += p[c] + q[c];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -442,10 +459,11 @@ bool get_encode() {
   return true;
 }
 
-// 2D fp32 row-major [rows][cols] map with a 32 x box_rows box, SWIZZLE_128B.
-bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int box_rows) {
+// 2D fp32 row-major [rows][cols] map (row stride ld elements, ld % 4 == 0) with a
+// 32 x box_rows box, SWIZZLE_128B; columns beyond cols read as zero.
+bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int ld, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
   cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es,
@@ -460,26 +478,27 @@ bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int box_rows) 
   return true;
 }
 
-template <int BN, int STAGES, int EPI, bool SPLITB>
-hrp_status launch(cudaStream_t st, const float* A, const float* B0, const float* B1, TcArgs a,
-                  int splits) {
-  CUtensorMap ma, mb0, mb1;
+template <int BN, int STAGES, int EPI>
+hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
+  CUtensorMap ma0, ma1, mb0, mb1;
   // boxes never exceed the tensor; rows of a tile beyond the box only feed masked outputs
   a.boxA = std::min(BM, a.M);
   a.boxB = std::min(BN, a.N);
-  if (!make_map(&ma, A, a.M, a.K, a.boxA) || !make_map(&mb0, B0, a.N, a.K, a.boxB)) return HRP_ECUDA;
-  if (!SPLITB && !make_map(&mb1, B1, a.N, a.K, a.boxB)) return HRP_ECUDA;
-  if (SPLITB) mb1 = mb0;
+  if (!make_map(&ma0, A.hi, a.M, a.K, a.lda, a.boxA) ||
+      !make_map(&ma1, A.lo, a.M, a.K, a.lda, a.boxA) ||
+      !make_map(&mb0, B.hi, a.N, a.K, a.ldb, a.boxB) ||
+      !make_map(&mb1, B.lo, a.N, a.K, a.ldb, a.boxB))
+    return HRP_ECUDA;
   constexpr int smem = TcSmem<BN, STAGES>::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI, SPLITB>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
     attr = true;
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, splits);
-  tc_gemm_kernel<BN, STAGES, EPI, SPLITB><<<grid, kThreadsTc, smem, st>>>(ma, mb0, mb1, a);
+  tc_gemm_kernel<BN, STAGES, EPI><<<grid, kThreadsTc, smem, st>>>(ma0, ma1, mb0, mb1, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
@@ -500,45 +519,55 @@ hrp_status tc_gemm_create(TcGemm** out, int device, int, const int*, int) {
 }
 void tc_gemm_destroy(TcGemm* g) { delete g; }
 
-bool tc_gemm_supported(int M, int N, int K) { return M >= 1 && N >= 1 && K >= 4 && K % 4 == 0; }
+bool tc_gemm_supported(int M, int N, int K) { return M >= 1 && N >= 1 && K >= 1; }
 
-static int pick_bn(int M, int N, int nsm) {
-  // the widest tile that still gives every SM a tile; narrow tiles for small problems
+int g_force_bn = 0;  // diagnostics: force the tile width (64 / 128 / 256), 0 = heuristic
+
+static int pick_bn(int M, int N, int K, int nsm) {
+  if (g_force_bn == 64 || g_force_bn == 128 || g_force_bn == 256) return g_force_bn;
+  // Cost model from the measured per-CTA times (profiles/diag_gemm.py, one CTA per SM):
+  // relative CTA time 1.0 / 1.31 / T256 for BN = 64 / 128 / 256 (BN = 256 runs 2 stages, so it
+  // slows down with K), times the number of waves; many-wave problems prefer the wide tiles
+  // (fewer operand re-reads from L2).
   const long mt = (M + BM - 1) / BM;
-  if (N > 128 && mt * ((N + 255) / 256) >= nsm) return 256;
-  if (N > 64 && mt * ((N + 127) / 128) >= nsm) return 128;
-  return 64;
+  const long t64 = mt * ((N + 63) / 64), t128 = mt * ((N + 127) / 128), t256 = mt * ((N + 255) / 256);
+  if (t64 > 4L * nsm) return K <= 512 ? 256 : 128;
+  const double T256 = K <= 256 ? 2.3 : (K <= 512 ? 2.8 : 3.0);
+  const double c64 = (double)((t64 + nsm - 1) / nsm);
+  const double c128 = 1.31 * (double)((t128 + nsm - 1) / nsm);
+  const double c256 = T256 * (double)((t256 + nsm - 1) / nsm);
+  if (c64 <= c128 && c64 <= c256) return 64;
+  return c128 <= c256 ? 128 : 256;
 }
 
-hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, const float* A,
-                       const float* Bh, const float* Bl, const float* bias, const float* aux,
-                       int ldaux, float* D, float* DT, int t_rows, unsigned long long* trace) {
+template <int EPI>
+static hrp_status run_bn(int bn, cudaStream_t st, Planes A, Planes B, const TcArgs& a) {
+  if (bn == 256) return launch<256, 2, EPI>(st, A, B, a, 1);
+  if (bn == 128) return launch<128, 3, EPI>(st, A, B, a, 1);
+  return launch<64, 4, EPI>(st, A, B, a, 1);
+}
+
+hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, Planes A,
+                       int lda, Planes B, int ldb, const float* bias, const float* aux, int ldaux,
+                       float* D, float* Dlo, float* DT, float* DTlo, int t_rows,
+                       unsigned long long* trace) {
   g->launches++;
   TcArgs a{};
   a.trace = trace;
   a.M = M; a.N = N; a.K = K; a.kc = K;
+  a.lda = lda; a.ldb = ldb;
   a.bias = bias; a.aux = aux; a.ldaux = ldaux;
-  a.D = D; a.ldd = N;
-  a.DT = DT; a.ldt = t_rows; a.t_rows = DT ? t_rows : 0;
-  const int bn = pick_bn(M, N, g->nsm);
-  if (bn == 256) {
-    if (epi == TC_EPI_BIAS) return launch<256, 2, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
-    if (epi == TC_EPI_BIAS_RELU) return launch<256, 2, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
-    return launch<256, 2, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
-  }
-  if (bn == 64) {
-    if (epi == TC_EPI_BIAS) return launch<64, 4, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
-    if (epi == TC_EPI_BIAS_RELU) return launch<64, 4, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
-    return launch<64, 4, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
-  }
-  if (epi == TC_EPI_BIAS) return launch<128, 3, TC_EPI_BIAS, false>(st, A, Bh, Bl, a, 1);
-  if (epi == TC_EPI_BIAS_RELU) return launch<128, 3, TC_EPI_BIAS_RELU, false>(st, A, Bh, Bl, a, 1);
-  return launch<128, 3, TC_EPI_RELU_MASK, false>(st, A, Bh, Bl, a, 1);
+  a.D = D; a.Dlo = Dlo; a.ldd = N;
+  a.DT = DT; a.DTlo = DT ? DTlo : nullptr; a.ldt = (t_rows + 3) / 4 * 4; a.t_rows = DT ? t_rows : 0;
+  const int bn = pick_bn(M, N, K, g->nsm);
+  if (epi == TC_EPI_BIAS) return run_bn<TC_EPI_BIAS>(bn, st, A, B, a);
+  if (epi == TC_EPI_BIAS_RELU) return run_bn<TC_EPI_BIAS_RELU>(bn, st, A, B, a);
+  return run_bn<TC_EPI_RELU_MASK>(bn, st, A, B, a);
 }
 
-hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, const float* A,
-                         const float* B, float* ws, size_t ws_elems, float* D) {
-  // D[M][N] = A[M][K] . B[N][K]^T, both raw (split in smem), split-K + deterministic reduce
+hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes A, Planes B,
+                         float* ws, size_t ws_elems, float* D) {
+  // D[M][N] = A[M][K] . B[N][K]^T, split-K + deterministic reduce
   const long tiles = (long)((M + BM - 1) / BM) * ((N + 127) / 128);
   int S = (int)std::max(1L, std::min(32L, (2L * g->nsm + tiles - 1) / tiles));
   int kc = (K + S - 1) / S;
@@ -547,9 +576,10 @@ hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, const 
   if ((size_t)S * M * N > ws_elems) { g_tc_err = "split-K workspace too small"; return HRP_ENOMEM; }
   TcArgs a{};
   a.M = M; a.N = N; a.K = K; a.kc = kc;
+  a.lda = K; a.ldb = K;
   a.D = S > 1 ? ws : D; a.ldd = N;
   g->launches++;
-  hrp_status s = launch<128, 3, TC_EPI_STORE, true>(st, A, B, nullptr, a, S);
+  hrp_status s = launch<128, 3, TC_EPI_STORE>(st, A, B, a, S);
   if (s || S == 1) return s;
   const int64_t n = (int64_t)M * N;
   reduce_splits_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(S, n, ws, D);
@@ -562,11 +592,12 @@ hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, const 
 hrp_status tc_split(TcGemm* g, cudaStream_t st, int rows, int cols, const float* w, float* hi,
                     float* lo, float* hiT, float* loT) {
   const int64_t n = (int64_t)rows * cols;
-  split_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(n, w, hi, lo);
+  split_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(
+      rows, cols, (cols + 3) / 4 * 4, w, hi, lo);
   g->launches++;
   if (hiT) {
     dim3 grid((cols + 31) / 32, (rows + 31) / 32);
-    split_t_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, w, hiT, loT);
+    split_t_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, (rows + 3) / 4 * 4, w, hiT, loT);
     g->launches++;
   }
   cudaError_t e = cudaGetLastError();
@@ -574,23 +605,26 @@ hrp_status tc_split(TcGemm* g, cudaStream_t st, int rows, int cols, const float*
   return HRP_OK;
 }
 
-hrp_status tc_transpose(TcGemm* g, cudaStream_t st, int rows, int cols, int ld_src,
-                        const float* src, int ld_dst, float* dst) {
-  dim3 grid((cols + 31) / 32, (rows + 31) / 32);
-  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, ld_src, src, ld_dst, dst);
+hrp_status tc_transpose(TcGemm* g, cudaStream_t st, int rows, int cols, int ld_src, Planes src,
+                        int ld_dst, float* dst_hi, float* dst_lo) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32, 2);
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(rows, cols, ld_src, src.hi, src.lo, ld_dst,
+                                                 dst_hi, dst_lo);
   g->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
 }
 
-hrp_status tc_rowsum(TcGemm* g, cudaStream_t st, int rows, int cols, const float* src, float* out) {
-  rowsum_kernel<<<(rows + 7) / 8, 256, 0, st>>>(rows, cols, src, out);
+hrp_status tc_rowsum(TcGemm* g, cudaStream_t st, int rows, int cols, Planes src, float* out) {
+  rowsum_kernel<<<(rows + 7) / 8, 256, 0, st>>>(rows, cols, src.hi, src.lo, out);
   g->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
 }
+
+void tc_gemm_force_bn(int bn) { g_force_bn = bn; }
 
 int tc_gemm_launches(TcGemm* g) {
   int n = g->launches;

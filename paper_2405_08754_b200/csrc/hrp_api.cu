@@ -205,6 +205,15 @@ hrp_status upload_tables(const HostSpace& hs, const hrp_profiles* prof, bool com
 
 }  // namespace
 
+// An activation-like buffer: raw fp32 (hi only, SIMT path) or split into tf32 hi / lo planes
+// (tensor-core path: every GEMM operand is written split by its producer).
+struct Pl {
+  float* hi = nullptr;
+  float* lo = nullptr;
+  Planes c() const { return Planes{hi, lo}; }
+  Pl off(size_t n) const { return Pl{hi + n, lo ? lo + n : nullptr}; }
+};
+
 struct hrp_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -213,7 +222,7 @@ struct hrp_ctx {
   // pair is CUDA-graph capturable.  Not used while per-kernel profiling is on.
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  std::vector<float*> act_t;          // target-pass hidden outputs [B][w] (concurrent scratch)
+  std::vector<Pl> act_t;              // target-pass hidden outputs [B][w] (concurrent scratch)
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   hrp_train_cfg cfg{};
@@ -230,8 +239,11 @@ struct hrp_ctx {
   // 3xTF32 operand splits for the tcgen05 GEMMs: [online hi | online lo | target hi | target lo]
   // in the flat parameter layout, and the online weights transposed ([in][out]) hi | lo.
   float *wsplit = nullptr, *wsplitT = nullptr;
-  std::vector<int64_t> soff;  // per-layer weight offsets in a split plane (128-B aligned for TMA)
+  // per-layer weight offsets in a split plane (128-B aligned for TMA): W [fo][r4(fi)] planes
+  // (soff) and W^T [fi][r4(fo)] planes (soffT)
+  std::vector<int64_t> soff, soffT;
   int64_t sstride = 0;        // floats per split plane
+  int ldX = 0, ldz = 0;       // row strides of X and dz (multiples of 4 on the tensor-core path)
   size_t ws_splitk_elems = 0;
   // env state
   uint8_t* win = nullptr;
@@ -245,17 +257,18 @@ struct hrp_ctx {
   int64_t t = 0, inserted = 0;
   // workspaces
   int rows_max = 0;
-  float* X = nullptr;                 // [rows][in]
-  std::vector<float*> act;            // hidden outputs [rows][w] per layer
+  Pl X;                               // [rows][in]
+  std::vector<Pl> act;                // hidden outputs [rows][w] per layer
   float* z = nullptr;                 // [rows][H]
   float* zt = nullptr;                // [B][H]
-  float* dz = nullptr;                // [B][H]
+  Pl dz;                              // [B][H]
   float *dh0 = nullptr, *dh1 = nullptr;  // [B][w] (SIMT backward ping-pong)
-  std::vector<float*> dhs, dhTs;      // tensor-core backward: per hidden layer dH, dH^T
-  // transposed operands of the tensor-core backward: X^T [in][B], hidden outputs^T [w][B],
-  // dz^T [H][B], dh^T [w][B]
-  float *XT = nullptr, *dzT = nullptr;
-  std::vector<float*> actT;
+  std::vector<Pl> dhs, dhTs;          // tensor-core backward: per hidden layer dH, dH^T
+  // transposed operands of the tensor-core backward (leading dimension Bp = B rounded up to 4,
+  // zero padding columns): X^T [in][Bp], hidden outputs^T [w][Bp], dz^T [H][Bp]
+  int Bp = 0;
+  Pl XT, dzT;
+  std::vector<Pl> actT;
   uint8_t* bwin = nullptr;            // [2B][W] or [chunk][W]
   uint64_t* bsched = nullptr;
   int64_t* bact = nullptr;
@@ -386,8 +399,8 @@ hrp_status split_weights(hrp_ctx* c, bool target) {
   for (int i = 0; i < nl; ++i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
     const int64_t o = c->woff[i], so = c->soff[i];
-    float* hT = target ? nullptr : c->wsplitT + so;
-    float* lT = target ? nullptr : c->wsplitT + c->sstride + so;
+    float* hT = target ? nullptr : c->wsplitT + c->soffT[i];
+    float* lT = target ? nullptr : c->wsplitT + c->sstride + c->soffT[i];
     prof_begin(c);
     hrp_status s = tc_split(c->tc, c->stream, fo, fi, th + o, hi + so, lo + so, hT, lT);
     if (s) return fail(s, tc_gemm_error());
@@ -399,60 +412,60 @@ hrp_status split_weights(hrp_ctx* c, bool target) {
 
 // Tensor-core GEMM D = epi(A . B^T) with pre-split B (hi, lo); optional transposed copy DT of
 // the first t_rows rows of D.
-hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, const float* A,
+hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, Planes A, int lda,
                   const float* Bh, const float* Bl, const float* bias, const float* aux, int ldaux,
-                  float* D, float* DT = nullptr, int t_rows = 0) {
+                  Pl D, Pl DT = Pl{}, int t_rows = 0) {
   prof_begin(c);
-  hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, Bh, Bl, bias, aux, ldaux, D, DT,
-                             t_rows);
+  hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, lda, Planes{Bh, Bl}, r4(K), bias,
+                             aux, ldaux, D.hi, D.lo, DT.hi, DT.lo, t_rows);
   if (s) return fail(s, tc_gemm_error());
   c->launches += tc_gemm_launches(c->tc) - 1;
   return launch_check(c, cls);
 }
 
-// Transposed copy dst [cols][rows] of src [rows][cols] (ld_src) on the tensor-core path.
-hrp_status transpose(hrp_ctx* c, int cls, int rows, int cols, int ld_src, const float* src,
-                     float* dst) {
+// Transposed copy dst [cols][ld_dst] of both planes of src [rows][cols] (ld_src).
+hrp_status transpose(hrp_ctx* c, int cls, int rows, int cols, int ld_src, Pl src, Pl dst,
+                     int ld_dst) {
   prof_begin(c);
-  hrp_status s = tc_transpose(c->tc, c->stream, rows, cols, ld_src, src, rows, dst);
+  hrp_status s = tc_transpose(c->tc, c->stream, rows, cols, ld_src, src.c(), ld_dst, dst.hi, dst.lo);
   if (s) return fail(s, tc_gemm_error());
   c->launches += tc_gemm_launches(c->tc) - 1;
   return launch_check(c, cls);
 }
 
-// The tensor-core backward needs B % 4 == 0 (TMA row stride of the transposed operands).
-bool tc_backward(const hrp_ctx* c, int B) { return c->gemm_mode == 2 && c->tc && B % 4 == 0; }
+bool tc_mode(const hrp_ctx* c) { return c->gemm_mode == 2 && c->tc; }
 
 // Forward of one network over M rows of X: hidden outputs to c->act (kept for the backward
-// pass), head output z_out [M][H].  With t_rows > 0 the first t_rows rows of every hidden
+// pass), head output z_out [M][H] (raw).  With t_rows > 0 the first t_rows rows of every hidden
 // output are also stored transposed in c->actT (operands of the weight-gradient GEMMs).
-hrp_status mlp_forward(hrp_ctx* c, const float* theta, const float* X, int M, float* z_out,
-                       int t_rows = 0, const std::vector<float*>* acts = nullptr) {
-  const std::vector<float*>& act = acts ? *acts : c->act;
+// Tensor-core path: X and the hidden outputs are hi/lo planes; SIMT path: raw (hi only).
+hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out,
+                       int t_rows = 0, const std::vector<Pl>* acts = nullptr) {
+  const std::vector<Pl>& act = acts ? *acts : c->act;
   c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
   const bool target = theta == c->theta_t;
-  const float* h = X;
+  Pl h = X;
+  int ldh = c->ldX;
   for (int i = 0; i < nl; ++i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
     const float* Wm = theta + c->woff[i];
     const float* b = Wm + (int64_t)fi * fo;
-    float* out = (i == nl - 1) ? z_out : act[i];
-    float* outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : nullptr;
+    const Pl out = (i == nl - 1) ? Pl{z_out, nullptr} : act[i];
     hrp_status s;
-    if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(M, fo, fi)) {
+    if (tc_mode(c)) {
+      const Pl outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : Pl{};
       const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
-      s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h, hi,
-                 hi + c->sstride, b, nullptr, 0, out, outT, t_rows);
+      s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h.c(),
+                 ldh, hi, hi + c->sstride, b, nullptr, 0, out, outT, t_rows);
+    } else if (i < nl - 1) {
+      s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h.hi, ldh, Wm, fi, out.hi, fo, b, nullptr, 0);
     } else {
-      if (i < nl - 1)
-        s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
-      else
-        s = sgemm<true, true, EPI_BIAS>(c, M, fo, fi, h, fi, Wm, fi, out, fo, b, nullptr, 0);
-      if (!s && outT) s = transpose(c, HRP_K_GEMM_FWD, t_rows, fo, fo, out, outT);
+      s = sgemm<true, true, EPI_BIAS>(c, M, fo, fi, h.hi, ldh, Wm, fi, out.hi, fo, b, nullptr, 0);
     }
     if (s) return s;
     h = out;
+    ldh = fo;
   }
   return HRP_OK;
 }
@@ -463,28 +476,29 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
   c->gemm_cls = HRP_K_GEMM_BWD;
   const int nl = (int)c->dims.size() - 1;
   const int H = c->dims[nl];
+  const int Bp = c->Bp;
   const bool conc = concurrent(c);
   hrp_status s;
-  if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, H, c->dz, c->dzT))) return s;
+  if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, c->ldz, c->dz, c->dzT, Bp))) return s;
   if (conc && (s = fork(c))) return s;
-  const float* dY = c->dz;
-  const float* dYT = c->dzT;
+  Pl dY = c->dz, dYT = c->dzT;
+  int ldy = c->ldz;
   for (int i = nl - 1; i >= 0; --i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
-    const float* HinT = (i == 0) ? c->XT : c->actT[i - 1];
-    const float* Hin = (i == 0) ? c->X : c->act[i - 1];
+    const Pl HinT = (i == 0) ? c->XT : c->actT[i - 1];
     float* gW = c->grad + c->woff[i];
     float* gb = gW + (int64_t)fi * fo;
-    // weight and bias gradients (side stream): dW [fo][fi] = dY^T . Hin = dYT . HinT^T
+    // weight and bias gradients (side stream): dW [fo][fi] = dY^T . Hin = dYT . HinT^T over the
+    // Bp (zero-padded) batch columns
     auto wgrad = [&]() -> hrp_status {
       prof_begin(c);
-      hrp_status t = tc_gemm_wgrad(c->tc, c->stream, fo, fi, B, dYT, HinT, c->ws_splitk,
+      hrp_status t = tc_gemm_wgrad(c->tc, c->stream, fo, fi, Bp, dYT.c(), HinT.c(), c->ws_splitk,
                                    c->ws_splitk_elems, gW);
       if (t) return fail(t, tc_gemm_error());
       c->launches += tc_gemm_launches(c->tc) - 1;
       if ((t = launch_check(c, HRP_K_GEMM_BWD))) return t;
       prof_begin(c);
-      t = tc_rowsum(c->tc, c->stream, fo, B, dYT, gb);
+      t = tc_rowsum(c->tc, c->stream, fo, Bp, dYT.c(), gb);
       if (t) return fail(t, tc_gemm_error());
       c->launches += tc_gemm_launches(c->tc) - 1;
       return launch_check(c, HRP_K_GEMM_BWD);
@@ -492,22 +506,15 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
     s = conc ? on_side(c, wgrad) : wgrad();
     if (s) return s;
     if (i > 0) {
-      // data gradient (main stream): dH = (dY . W) * ReLU'(Hin), and its transpose
-      float* dH = c->dhs[i - 1];
-      float* dHT = c->dhTs[i - 1];
-      if (tc_gemm_supported(B, fi, fo)) {
-        const float* hT = c->wsplitT + c->soff[i];
-        s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->sstride,
-                   nullptr, Hin, fi, dH, dHT, B);
-      } else {
-        const float* Wm = c->theta + c->woff[i];
-        s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
-        if (!s) s = transpose(c, HRP_K_GEMM_BWD, B, fi, fi, dH, dHT);
-      }
+      // data gradient (main stream): dH = (dY . W) * ReLU'(Hin), split, and its transpose
+      const float* hT = c->wsplitT + c->soffT[i];
+      s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY.c(), ldy, hT,
+                 hT + c->sstride, nullptr, c->act[i - 1].hi, fi, c->dhs[i - 1], c->dhTs[i - 1], B);
       if (s) return s;
       if (conc && (s = fork(c))) return s;
-      dY = dH;
-      dYT = dHT;
+      dY = c->dhs[i - 1];
+      dYT = c->dhTs[i - 1];
+      ldy = fi;
     }
   }
   if (conc && (s = join(c))) return s;
@@ -515,20 +522,22 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
 }
 
 // Backward over the first B rows (X rows [0,B), act rows [0,B)), dz [B][H] -> c->grad.
+// SIMT path: raw buffers.
 hrp_status mlp_backward(hrp_ctx* c, int B) {
-  if (tc_backward(c, B)) return mlp_backward_tc(c, B);
+  if (tc_mode(c)) return mlp_backward_tc(c, B);
   c->gemm_cls = HRP_K_GEMM_BWD;
   const int nl = (int)c->dims.size() - 1;
-  const float* dY = c->dz;
+  const float* dY = c->dz.hi;
   float* bufs[2] = {c->dh0, c->dh1};
   int cur = 0;
   for (int i = nl - 1; i >= 0; --i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
-    const float* Hin = (i == 0) ? c->X : c->act[i - 1];
+    const float* Hin = (i == 0) ? c->X.hi : c->act[i - 1].hi;
+    const int ldin = (i == 0) ? c->ldX : fi;
     float* gW = c->grad + c->woff[i];
     float* gb = gW + (int64_t)fi * fo;
     // dW = dY^T . Hin  ([fo][fi]); reduction over the batch
-    hrp_status s = sgemm<false, false, EPI_STORE>(c, fo, fi, B, dY, fo, Hin, fi, gW, fi,
+    hrp_status s = sgemm<false, false, EPI_STORE>(c, fo, fi, B, dY, fo, Hin, ldin, gW, fi,
                                                   nullptr, nullptr, 0);
     if (s) return s;
     prof_begin(c);
@@ -537,14 +546,7 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     if (i > 0) {
       const float* Wm = c->theta + c->woff[i];
       float* dH = bufs[cur];
-      if (c->gemm_mode == 2 && c->tc && tc_gemm_supported(B, fi, fo)) {
-        // dH = dY . W = dY . (W^T)^T with the transposed online split as the B operand
-        const float* hT = c->wsplitT + c->soff[i];
-        s = tc_run(c, HRP_K_GEMM_BWD, TC_EPI_RELU_MASK, B, fi, fo, dY, hT, hT + c->sstride,
-                   nullptr, Hin, fi, dH);
-      } else {
-        s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
-      }
+      s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
       if (s) return s;
       dY = dH;
       cur ^= 1;
@@ -720,12 +722,14 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   }
   c->n_params = o;
   {
-    int64_t so = 0;
+    int64_t so = 0, st = 0;
     for (size_t i = 0; i + 1 < c->dims.size(); ++i) {
       c->soff.push_back(so);
-      so += ((int64_t)c->dims[i] * c->dims[i + 1] + 31) / 32 * 32;
+      c->soffT.push_back(st);
+      so += ((int64_t)c->dims[i + 1] * r4(c->dims[i]) + 31) / 32 * 32;
+      st += ((int64_t)c->dims[i] * r4(c->dims[i + 1]) + 31) / 32 * 32;
     }
-    c->sstride = so;
+    c->sstride = std::max(so, st);
   }
   const int E = cfg->n_envs, B = cfg->batch, W = hs.W, H = hs.head_width();
   const int in = c->dims[0], wd = cfg->hidden_width;
@@ -750,29 +754,44 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->rep_act, N * 8));
   CK(ar.alloc((void**)&c->rep_r, N * 4));
   CK(ar.alloc((void**)&c->rep_done, N));
-  CK(ar.alloc((void**)&c->X, sizeof(float) * R * in));
-  for (int i = 0; i < cfg->hidden_layers; ++i) {
-    float* p;
-    CK(ar.alloc((void**)&p, sizeof(float) * R * wd));
-    c->act.push_back(p);
-  }
+  const bool split = c->gemm_mode == 2;   // tensor-core path: operands stored as hi/lo planes
+  c->Bp = r4(B);
+  c->ldX = split ? r4(in) : in;
+  c->ldz = split ? r4(H) : H;
+  const size_t Bp = c->Bp;
+  auto alloc_pl = [&](Pl& p, size_t n, bool two) -> cudaError_t {
+    cudaError_t e = ar.alloc((void**)&p.hi, sizeof(float) * n);
+    if (e == cudaSuccess && two) e = ar.alloc((void**)&p.lo, sizeof(float) * n);
+    return e;
+  };
+  CK(alloc_pl(c->X, R * c->ldX, split));
+  c->act.resize(cfg->hidden_layers);
+  for (auto& p : c->act) CK(alloc_pl(p, R * wd, split));
   CK(ar.alloc((void**)&c->z, sizeof(float) * R * H));
   CK(ar.alloc((void**)&c->zt, sizeof(float) * (size_t)B * H));
-  CK(ar.alloc((void**)&c->dz, sizeof(float) * (size_t)B * H));
+  CK(alloc_pl(c->dz, (size_t)B * c->ldz, split));
   CK(ar.alloc((void**)&c->dh0, sizeof(float) * (size_t)B * wd));
   CK(ar.alloc((void**)&c->dh1, sizeof(float) * (size_t)B * wd));
-  CK(ar.alloc((void**)&c->XT, sizeof(float) * (size_t)B * in));
-  CK(ar.alloc((void**)&c->dzT, sizeof(float) * (size_t)B * H));
-  for (int i = 0; i < cfg->hidden_layers; ++i) {
-    float *p, *q, *u, *v;
-    CK(ar.alloc((void**)&p, sizeof(float) * (size_t)B * wd));
-    CK(ar.alloc((void**)&q, sizeof(float) * (size_t)B * wd));
-    CK(ar.alloc((void**)&u, sizeof(float) * (size_t)B * wd));
-    CK(ar.alloc((void**)&v, sizeof(float) * (size_t)B * wd));
-    c->actT.push_back(p);
-    c->act_t.push_back(q);
-    c->dhs.push_back(u);
-    c->dhTs.push_back(v);
+  c->act_t.resize(cfg->hidden_layers);
+  for (auto& p : c->act_t) CK(alloc_pl(p, (size_t)B * wd, split));
+  if (split) {
+    // transposed operands: zero padding columns [B, Bp) are never written
+    CK(alloc_pl(c->XT, Bp * in, true));
+    CK(alloc_pl(c->dzT, Bp * H, true));
+    CK(cudaMemsetAsync(c->XT.hi, 0, sizeof(float) * Bp * in, c->stream));
+    CK(cudaMemsetAsync(c->XT.lo, 0, sizeof(float) * Bp * in, c->stream));
+    CK(cudaMemsetAsync(c->dzT.hi, 0, sizeof(float) * Bp * H, c->stream));
+    CK(cudaMemsetAsync(c->dzT.lo, 0, sizeof(float) * Bp * H, c->stream));
+    c->actT.resize(cfg->hidden_layers);
+    c->dhs.resize(cfg->hidden_layers);
+    c->dhTs.resize(cfg->hidden_layers);
+    for (int i = 0; i < cfg->hidden_layers; ++i) {
+      CK(alloc_pl(c->actT[i], Bp * wd, true));
+      CK(alloc_pl(c->dhs[i], (size_t)B * wd, true));
+      CK(alloc_pl(c->dhTs[i], Bp * wd, true));
+      for (float* q : {c->actT[i].hi, c->actT[i].lo, c->dhTs[i].hi, c->dhTs[i].lo})
+        CK(cudaMemsetAsync(q, 0, sizeof(float) * Bp * wd, c->stream));
+    }
   }
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -861,7 +880,8 @@ hrp_status hrp_env_step(hrp_ctx* c, uint64_t thr, const uint32_t* d_u_explore,
   const int E = c->cfg.n_envs;
   hrp_status s;
   prof_begin(c);
-  encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool, c->X);
+  encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool, c->X.hi,
+                                                     c->X.lo, c->ldX);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
   if ((s = mlp_forward(c, c->theta, c->X, E, c->z))) return s;
   SelArgs a{};
@@ -906,7 +926,8 @@ hrp_status hrp_q_forward(hrp_ctx* c, int64_t n, const uint8_t* d_windows, const 
     const uint8_t* wp = d_windows + r0 * W;
     const uint64_t* sp = d_sched + r0;
     prof_begin(c);
-    encode_kernel<<<(M + 7) / 8, 256, 0, c->stream>>>(M, W, wp, sp, c->dt.pool, c->X);
+    encode_kernel<<<(M + 7) / 8, 256, 0, c->stream>>>(M, W, wp, sp, c->dt.pool, c->X.hi, c->X.lo,
+                                                       c->ldX);
     if ((s = launch_check(c, HRP_K_ENCODE))) return s;
     float* zo = d_head ? d_head + r0 * H : c->z;
     if ((s = mlp_forward(c, c->theta, c->X, M, zo))) return s;
@@ -939,16 +960,17 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   if ((s = launch_check(c, HRP_K_SAMPLE))) return s;
   prof_begin(c);
   encode_kernel<<<(2 * B + 7) / 8, 256, 0, c->stream>>>(2 * B, c->hs.W, c->bwin, c->bsched,
-                                                         c->dt.pool, c->X);
+                                                         c->dt.pool, c->X.hi, c->X.lo, c->ldX);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
-  const bool tcb = tc_backward(c, B);
-  if (tcb && (s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->dims[0], c->X, c->XT))) return s;
+  const bool tcb = tc_mode(c);
+  if (tcb && (s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->ldX, c->X, c->XT, c->Bp)))
+    return s;
   // online net on [s; s'] (activations of the s rows kept for backward) on the main stream,
   // target net on s' beside it (its own activation scratch)
   const bool conc = concurrent(c);
   if (conc && (s = fork(c))) return s;
   auto target_pass = [&]() {
-    return mlp_forward(c, c->theta_t, c->X + (size_t)B * c->dims[0], B, c->zt, 0, &c->act_t);
+    return mlp_forward(c, c->theta_t, c->X.off((size_t)B * c->ldX), B, c->zt, 0, &c->act_t);
   };
   if (conc) {
     if ((s = on_side(c, target_pass))) return s;
@@ -970,7 +992,9 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.gamma = c->cfg.gamma;
   t.inv_btot = 1.f / ((float)B * (float)c->world);
   t.explicit_mode = c->explicit_mode;
-  t.dz = c->dz;
+  t.dz = c->dz.hi;
+  t.dz_lo = c->dz.lo;
+  t.ldz = c->ldz;
   t.dsq = c->dsq;
   t.astar = d_astar;
   t.n_evals = c->n_evals + 1;
@@ -995,11 +1019,35 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
     if ((s = launch_check(c, HRP_K_ALLREDUCE))) return s;
   }
   prof_begin(c);
-  sgd_kernel<<<4 * 148, 256, 0, c->stream>>>(c->n_params, c->cfg.lr, c->theta, c->grad, c->theta_t,
-                                              sync_target);
+  if (tc_mode(c)) {
+    SgdSplitArgs g{};
+    g.nl = (int)c->dims.size() - 1;
+    g.n = c->n_params;
+    g.lr = c->cfg.lr;
+    g.th = c->theta;
+    g.g = c->grad;
+    g.tgt = c->theta_t;
+    g.sync = sync_target;
+    g.hi = c->wsplit;
+    g.lo = c->wsplit + c->sstride;
+    g.thi = c->wsplit + 2 * c->sstride;
+    g.tlo = c->wsplit + 3 * c->sstride;
+    g.hiT = c->wsplitT;
+    g.loT = c->wsplitT + c->sstride;
+    for (int i = 0; i < g.nl; ++i) {
+      g.woff[i] = c->woff[i];
+      g.soff[i] = c->soff[i];
+      g.soffT[i] = c->soffT[i];
+      g.fi[i] = c->dims[i];
+      g.fo[i] = c->dims[i + 1];
+    }
+    g.woff[g.nl] = c->n_params;
+    sgd_split_kernel<<<8 * 148, 256, 0, c->stream>>>(g);
+  } else {
+    sgd_kernel<<<4 * 148, 256, 0, c->stream>>>(c->n_params, c->cfg.lr, c->theta, c->grad,
+                                                c->theta_t, sync_target);
+  }
   if ((s = launch_check(c, HRP_K_SGD))) return s;
-  if ((s = split_weights(c, false))) return s;
-  if (sync_target && (s = split_weights(c, true))) return s;
   (void)H;
   return HRP_OK;
 }
@@ -1117,21 +1165,45 @@ hrp_status hrp_set_weights(hrp_ctx* c, const float* in) {
 }
 
 hrp_status hrp_diag_gemm(int device, void* cuda_stream, int M, int N, int K, const float* d_A,
-                         const float* d_W, const float* d_bias, float* d_D, uint64_t* d_trace) {
+                         const float* d_W, const float* d_bias, float* d_D, uint64_t* d_trace,
+                         int reps, int force_bn, float* ms_out) {
   if (!d_A || !d_W || !d_bias || !d_D) return fail(HRP_EINVAL, "NULL argument");
-  if (!tc_gemm_supported(M, N, K)) return fail(HRP_ERANGE, "shape not supported (K % 4)");
+  if (!tc_gemm_supported(M, N, K)) return fail(HRP_ERANGE, "shape not supported");
   CK(cudaSetDevice(device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   TcGemm* g = nullptr;
   hrp_status s = tc_gemm_create(&g, device, M, nullptr, 0);
   if (s) return fail(s, tc_gemm_error());
   float* split = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&split, sizeof(float) * 2 * (size_t)N * K, st);
+  const size_t nw = (size_t)N * r4(K), na = (size_t)M * r4(K);
+  cudaError_t e = cudaMallocAsync((void**)&split, sizeof(float) * 2 * (nw + na), st);
   if (e != cudaSuccess) { tc_gemm_destroy(g); return fail(HRP_ENOMEM, cudaGetErrorString(e)); }
-  s = tc_split(g, st, N, K, d_W, split, split + (size_t)N * K, nullptr, nullptr);
-  if (!s)
-    s = tc_gemm_run(g, st, TC_EPI_BIAS, M, N, K, d_A, split, split + (size_t)N * K, d_bias,
-                    nullptr, 0, d_D, nullptr, 0, reinterpret_cast<unsigned long long*>(d_trace));
+  float* ah = split + 2 * nw;
+  s = tc_split(g, st, N, K, d_W, split, split + nw, nullptr, nullptr);
+  if (!s) s = tc_split(g, st, M, K, d_A, ah, ah + na, nullptr, nullptr);
+  tc_gemm_force_bn(force_bn);
+  auto run = [&](unsigned long long* tr) {
+    return tc_gemm_run(g, st, TC_EPI_BIAS, M, N, K, Planes{ah, ah + na}, r4(K),
+                       Planes{split, split + nw}, r4(K), d_bias, nullptr, 0, d_D, nullptr,
+                       nullptr, nullptr, 0, tr);
+  };
+  if (!s) s = run(reinterpret_cast<unsigned long long*>(d_trace));
+  if (!s && reps > 0 && ms_out) {
+    // kernel-only time: reps back-to-back launches between two events
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    for (int r = 0; r < reps && !s; ++r) s = run(nullptr);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ms_out = ms / (float)reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  tc_gemm_force_bn(0);
   cudaFreeAsync(split, st);
   tc_gemm_destroy(g);
   if (s) return fail(s, tc_gemm_error());

@@ -12,9 +12,10 @@ namespace hrp {
 // ---------------------------------------------------------------------------------------
 // a2: x[row] = W rows of [features(12) | c/cbar, m/mbar, T/Tbar | scheduled | U/W]
 // One warp per state.
+// X is written raw, or (Xlo != NULL) split into tf32 hi / lo planes for the tensor-core GEMMs.
 __global__ void encode_kernel(int M, int W, const uint8_t* __restrict__ win,
                               const uint64_t* __restrict__ sched, DevPool pool,
-                              float* __restrict__ X) {
+                              float* __restrict__ X, float* __restrict__ Xlo, int ldx) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int in = W * 17;
@@ -37,7 +38,8 @@ __global__ void encode_kernel(int M, int W, const uint8_t* __restrict__ win,
     const int U = W - __popcll(s);
     const float fW = (float)W;
     const float ic = fW / (float)sc, im = fW / (float)sm, iT = fW / (float)sT;
-    float* x = X + (size_t)row * in;
+    float* x = X + (size_t)row * ldx;
+    float* xl = Xlo ? Xlo + (size_t)row * ldx : nullptr;
     for (int i = lane; i < in; i += 32) {
       const int j = i / 17, col = i - j * 17;
       const int p = w[j];
@@ -48,7 +50,13 @@ __global__ void encode_kernel(int M, int W, const uint8_t* __restrict__ win,
       else if (col == 14) v = (float)pool.T[p] * iT;
       else if (col == 15) v = (float)((s >> j) & 1ull);
       else v = (float)U / fW;
-      x[i] = v;
+      if (xl) {
+        const float h = tf32_rna(v);
+        x[i] = h;
+        xl[i] = v - h;
+      } else {
+        x[i] = v;
+      }
     }
   }
 }
@@ -210,7 +218,9 @@ struct TdArgs {
   float gamma;
   float inv_btot;       // 1 / (B * world)
   bool explicit_mode;
-  float* dz;            // [B][H]
+  float* dz;            // [B][H] raw, or the hi plane when dz_lo != NULL
+  float* dz_lo;         // [B][H] lo plane (tensor-core path) or NULL
+  int ldz;              // row stride of dz
   float* dsq;           // [B]
   int64_t* astar;       // [B] optional
   unsigned long long* n_evals;
@@ -225,6 +235,52 @@ __global__ void sgd_kernel(int64_t n, float lr, float* __restrict__ th, const fl
     const float v = th[i] - lr * g[i];
     th[i] = v;
     if (sync) tgt[i] = v;
+  }
+}
+
+// a13 on the tensor-core path, one launch: theta -= lr * g, the 3xTF32 hi / lo planes of every
+// weight matrix re-split from the new value (W [fo][ldw] and W^T [fi][ldt] planes), and on a
+// target-sync step the target parameters and their planes too (identical values).
+constexpr int kMaxLayers = 9;
+struct SgdSplitArgs {
+  int nl;
+  int64_t n;                         // parameters
+  float lr;
+  float* th;
+  const float* g;
+  float* tgt;                        // target parameters (written iff sync)
+  int sync;
+  float *hi, *lo;                    // online W planes
+  float *thi, *tlo;                  // target W planes (written iff sync)
+  float *hiT, *loT;                  // online W^T planes
+  int64_t woff[kMaxLayers + 1];      // flat offsets (woff[nl] = n)
+  int64_t soff[kMaxLayers], soffT[kMaxLayers];
+  int fi[kMaxLayers], fo[kMaxLayers];
+};
+
+__global__ void sgd_split_kernel(SgdSplitArgs a) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = a.th[i] - a.lr * a.g[i];
+    a.th[i] = v;
+    if (a.sync) a.tgt[i] = v;
+    int l = 0;
+    while (l + 1 < a.nl && i >= a.woff[l + 1]) ++l;
+    const int64_t q = i - a.woff[l];
+    const int fi = a.fi[l], fo = a.fo[l];
+    if (q >= (int64_t)fi * fo) continue;  // bias: used raw by the GEMM epilogue
+    const int r = (int)(q / fi), cc = (int)(q - (int64_t)r * fi);
+    const float h = tf32_rna(v), lw = v - h;
+    const int64_t o = a.soff[l] + (int64_t)r * ((fi + 3) & ~3) + cc;
+    a.hi[o] = h;
+    a.lo[o] = lw;
+    if (a.sync) {
+      a.thi[o] = h;
+      a.tlo[o] = lw;
+    }
+    const int64_t ot = a.soffT[l] + (int64_t)cc * ((fo + 3) & ~3) + r;
+    a.hiT[ot] = h;
+    a.loT[ot] = lw;
   }
 }
 

@@ -753,7 +753,8 @@ __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) t
     }
     const float sc = delta * a.inv_btot;
     const float invL = 1.f / (float)L, invW = 1.f / (float)W;
-    float* dzr = a.dz + (size_t)b * H;
+    float* dzr = a.dz + (size_t)b * a.ldz;
+    float* dzl = a.dz_lo ? a.dz_lo + (size_t)b * a.ldz : nullptr;
     // dQ/dz: v -> 1; aL[l'] -> [l' = l] - 1/L; aJ[j][t] -> #{i: g_i = j, t_i = t} - #{i: t_i = t}/W
     for (int h = lane; h < H; h += 32) {
       float dv;
@@ -769,7 +770,14 @@ __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) t
         }
         dv = (float)cjt - (float)ct * invW;
       }
-      dzr[h] = dv * sc;
+      const float g = dv * sc;
+      if (dzl) {
+        const float hh = tf32_rna(g);
+        dzr[h] = hh;
+        dzl[h] = g - hh;
+      } else {
+        dzr[h] = g;
+      }
     }
     __syncwarp();
   }
