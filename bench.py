@@ -395,6 +395,200 @@ def dominant(rl):
             "share_of_step": None}
 
 
+# ------------------------------------------------------------------------------------------
+# Supplementary lines (not the driver's headline): BASELINE config 3 (exhaustive brute-force
+# optimum, a14) and config 5 (inference-only Q scoring, a2-a5 in SEL_INFER mode).
+
+def _timed_calls(fn, steps, warmup, stream, flush):
+    import torch
+    for _ in range(warmup):
+        fn()
+    stream.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    for e0, e1 in ev:
+        flush.zero_()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+    stream.synchronize()
+    return sum(a.elapsed_time(b) for a, b in ev)
+
+
+def run_brute(args, cfg):
+    """Config 3: hrp_bruteforce_optimum over Q1-Q12 (Table V) + 4096 random windows per call."""
+    import torch
+    from paper_2405_08754_b200 import hrp
+    from paper_2405_08754_b200.session import space_of
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    pool = synth.make_pool(cfg.pool)
+    sc = cfg.space
+    wins = np.concatenate([synth.table_v_windows(pool),
+                           synth.make_windows(pool, cfg.n_windows, sc.window, step=1)])
+    n, W = wins.shape
+    space, prof = space_of(sc), hrp.make_profiles(pool)
+    tab = hrp.hrp_layout_table(space)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(stream):
+        w = torch.from_numpy(wins).to(dev)
+        best = torch.empty(n, dtype=torch.int64, device=dev)
+        solo = torch.empty(n, dtype=torch.int64, device=dev)
+        rgs = torch.empty((n, W), dtype=torch.uint8, device=dev)
+        bact = torch.empty((n, W), dtype=torch.int64, device=dev)
+
+        def call():
+            hrp.hrp_bruteforce_optimum(space, prof, n, w, best, solo, rgs, bact, stream.cuda_stream)
+        clocks = Clocks(local)
+        ms = _timed_calls(call, args.steps, args.warmup, stream, flush)
+        clk = clocks.stop()
+        # e2e: windows from pinned host memory in, results out, inside the timed region
+        wh = torch.from_numpy(wins).pin_memory()
+        oh = [torch.empty(n, dtype=torch.int64).pin_memory(),
+              torch.empty((n, W), dtype=torch.uint8).pin_memory()]
+
+        def call_e2e():
+            w.copy_(wh, non_blocking=True)
+            call()
+            oh[0].copy_(best, non_blocking=True)
+            oh[1].copy_(rgs, non_blocking=True)
+        ms_e2e = _timed_calls(call_e2e, args.steps, 1, stream, flush)
+    # algorithmic work: (job set, layout, slot permutation) evaluations of phase 1
+    from math import comb, factorial
+    nc = np.bincount(np.asarray(tab["nslots"]), minlength=5)
+    evals = sum(comb(W, c) * int(nc[c]) * factorial(c) for c in range(1, 5))
+    slot_terms = sum(comb(W, c) * int(nc[c]) * factorial(c) * c for c in range(1, 5))
+    sec = ms / 1e3
+    value = n * args.steps / sec
+    pk = _peaks()
+    alu_peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    ach = slot_terms * n * args.steps / sec / 1e12
+    res = {"metric": "brute-force optimum windows/s (BASELINE config 3)", "value": value,
+           "unit": "windows/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "i64", "data": "synthetic",
+           "config": {"workload": f"cfg3: W={W}, Cmax={sc.cmax}, MIG GI/CI x MPS "
+                                  f"{{{min(sc.shares)}..{max(sc.shares)}}}%, Q1-Q12 (Table V) + "
+                                  f"{cfg.n_windows} random windows per call",
+                      "windows_per_call": n, "evals_per_window": evals,
+                      "l2": "flushed (256 MiB memset) between timed calls"},
+           "gpu_launches": 1,
+           "e2e": {"value": n * args.steps / (ms_e2e / 1e3), "unit": "windows/s",
+                   "h2d_bytes_per_step": int(wins.nbytes),
+                   "d2h_bytes_per_step": int(n * 8 + n * W)},
+           "clocks": clk,
+           "roofline": {"kernel": "brute_kernel", "bound": "alu", "achieved": ach,
+                        "peak": alu_peak, "unit": "Tops/s", "frac": ach / alu_peak,
+                        "traffic": None,
+                        "work": f"{slot_terms} slot terms per window (one lane-op each, a lower "
+                                f"bound on the integer work of {evals} (set, layout, sigma) "
+                                f"evaluations)",
+                        "peak_src": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)"}}
+    if not args.no_cpu_baseline:
+        from oracle import brute as BR
+        from oracle import space as SP
+        osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
+        t0 = time.perf_counter()
+        k = 0
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            BR.dp_opt(osp, [int(x) for x in wins[k % n]], pool)
+            k += 1
+        dt = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": k / dt, "unit": "windows/s", "cores": 1,
+                               "kind": "oracle",
+                               "sample": f"{k} windows through oracle.brute.dp_opt, 1 thread, "
+                                         f"{dt:.1f} s"}
+    print(json.dumps(res), flush=True)
+
+
+def run_infer(args, cfg):
+    """Config 5: inference-only Q scoring (hrp_q_forward) of cfg.n_states job-mix states per
+    call; states sharded across ranks (replicas only, no collective)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2405_08754_b200 import hrp, parallel
+    from paper_2405_08754_b200.session import Session
+    rank, world, local = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(dev)
+    pool = synth.make_pool(cfg.pool)
+    n = cfg.n_states // world
+    chunk = 65536
+    base = synth.config(2)
+    ecfg = base.with_(n_envs=chunk, batch=chunk)
+    from oracle import qnet as QN
+    from oracle import space as SP
+    sc = cfg.space
+    osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
+    th = synth.init_weights(QN.net_dims(osp, cfg.net))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(stream):
+        sess = Session(ecfg, pool, init_weights=th, device=local, stream=stream, replay=chunk)
+        wins = synth.make_windows(pool, n, sc.window, step=5, rank=rank)
+        sched = synth.sched_states(n, sc.window, rank=rank)
+        wd = torch.from_numpy(wins).to(dev)
+        sd = torch.from_numpy(sched.view(np.int64)).to(dev)
+        am = torch.empty(n, dtype=torch.int64, device=dev)
+        qm = torch.empty(n, dtype=torch.float32, device=dev)
+
+        def call():
+            hrp.hrp_q_forward(sess.ctx, n, wd, sd, am, qm, None)
+        e0 = hrp.hrp_eval_counts(sess.ctx)
+        l0 = sess.launches()
+        clocks = Clocks(local)
+        ms = _timed_calls(call, args.steps, args.warmup, stream, flush)
+        clk = clocks.stop()
+        e1 = hrp.hrp_eval_counts(sess.ctx)
+        launches = (sess.launches() - l0) / (args.steps + args.warmup)
+        evals = (e1[0] - e0[0]) / (args.steps + args.warmup)
+        wh = torch.from_numpy(wins).pin_memory()
+        sh = torch.from_numpy(sched.view(np.int64)).pin_memory()
+        ah = torch.empty(n, dtype=torch.int64).pin_memory()
+        qh = torch.empty(n, dtype=torch.float32).pin_memory()
+
+        def call_e2e():
+            wd.copy_(wh, non_blocking=True)
+            sd.copy_(sh, non_blocking=True)
+            call()
+            ah.copy_(am, non_blocking=True)
+            qh.copy_(qm, non_blocking=True)
+        ms_e2e = _timed_calls(call_e2e, args.steps, 1, stream, flush)
+        sess.close()
+    ms = parallel.max_over_ranks(ms, dev) if world > 1 else ms
+    ms_e2e = parallel.max_over_ranks(ms_e2e, dev) if world > 1 else ms_e2e
+    if rank == 0:
+        sec = ms / 1e3
+        res = {"metric": "Q-evals/s (inference-only Q scoring, BASELINE config 5)",
+               "value": evals * world * args.steps / sec, "unit": "Q-evals/s",
+               "states_per_s": n * world * args.steps / sec,
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32+i64", "data": "synthetic",
+               "config": {"workload": f"cfg5: {cfg.n_states} job-mix states x full action space "
+                                      f"(W={sc.window}, Cmax={sc.cmax}, Q-MLP "
+                                      f"{cfg.net.hidden_layers}x{cfg.net.hidden_width}), "
+                                      f"{chunk}-row chunks", "states_per_call": n * world,
+                          "argmax": "explicit (every valid action scored)",
+                          "parallelism": f"replicas x{world} (states sharded, no collective)",
+                          "l2": "flushed (256 MiB memset) between timed calls"},
+               "gpu_launches": int(round(launches * args.steps)),
+               "e2e": {"value": evals * world * args.steps / (ms_e2e / 1e3), "unit": "Q-evals/s",
+                       "h2d_bytes_per_step": int(wins.nbytes + sched.nbytes),
+                       "d2h_bytes_per_step": int(n * 12)},
+               "clocks": clk}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -412,6 +606,10 @@ def main():
     cfg = synth.config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.n_windows:
+        run_brute(args, cfg)
+    elif cfg.n_states:
+        run_infer(args, cfg)
     else:
         run_gpu(args, cfg)
 

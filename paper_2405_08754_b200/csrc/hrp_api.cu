@@ -1069,6 +1069,26 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   if (hs.W > kBruteMaxW) return fail(HRP_ERANGE, "brute force supports W <= 12");
   if (hs.L > 512) return fail(HRP_ERANGE, "brute force supports <= 512 layouts");
   if (hs.n_actions() >= (int64_t(1) << kBruteIdxBits)) return fail(HRP_ERANGE, "|A| >= 2^26");
+  // distinct memory sizes of the layout slots (the per-window memory-term table has a column
+  // per size) and the range of that table (uint32)
+  int nb8 = 0, b8v[kBruteMaxB8] = {0, 0, 0, 0};
+  for (int l = 0; l < hs.L; ++l)
+    for (int k = 0; k < hs.nslots[l]; ++k) {
+      const int b = hs.slots[l][k].b8;
+      bool seen = false;
+      for (int q = 0; q < nb8; ++q) seen |= b8v[q] == b;
+      if (!seen) {
+        if (nb8 == kBruteMaxB8) return fail(HRP_ERANGE, "brute force: more than 4 memory sizes");
+        b8v[nb8++] = b;
+      }
+    }
+  {
+    int64_t tmax = 0;
+    for (int i = 0; i < prof->n_jobs; ++i) tmax = std::max<int64_t>(tmax, prof->solo_ticks[i]);
+    // memory term <= Tmax * Cmax * 1000 * (8 + q (Cmax - 1)) / 1000 (demand <= 1000 permille)
+    const double bound = (double)tmax * hs.cmax * (8.0 + (double)space->interference_q3 * (hs.cmax - 1));
+    if (bound >= 4294967296.0) return fail(HRP_ERANGE, "brute force: solo ticks too large");
+  }
   if (n == 0) return HRP_OK;
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -1089,7 +1109,7 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brute_kernel, 512, smem);
   const int grid = (int)std::min<int64_t>(n, (int64_t)nsm * std::max(1, occ));
-  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact};
+  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact, nb8, {b8v[0], b8v[1], b8v[2], b8v[3]}};
   brute_kernel<<<grid, 512, smem, st>>>(dt.sp, dt.pool, a);
   e = cudaGetLastError();
   cudaError_t e2 = cudaStreamSynchronize(st);

@@ -46,7 +46,8 @@ struct PWarpSmem {
   float* meanJ;   // [T] slot-type means of the job advantages
   int* top;       // pruned: [T][4] Top-C positions
   int64_t* topv;  // pruned: [T][4] their F values
-  float* cj;      // explicit: [T][kXRows] centred job advantages of the free positions (type-major)
+  float* cj;      // explicit: [T][kXRows] centred job advantages of the free positions (type-major),
+                  // followed by sf [T][kXRows]: suffix maxima sf[t][r] = max_{r' >= r} cj[t][r']
   int* pos;       // explicit: [U] free window positions, ascending
 };
 
@@ -61,7 +62,7 @@ struct PTabs {
 __host__ __device__ inline size_t pwarp_bytes(int T, int H, bool x) {
   size_t b = align16(sizeof(float) * T);
   if (x)
-    b += align16(sizeof(float) * kXRows * T) + align16(sizeof(int) * kXMaxW);
+    b += align16(sizeof(float) * 2 * kXRows * T) + align16(sizeof(int) * kXMaxW);
   else
     b += align16(sizeof(int) * T * 4) + align16(sizeof(int64_t) * T * 4);
   return b;
@@ -109,7 +110,7 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
   w.pos = nullptr;
   if (X > 0) {
     w.cj = (float*)wb;
-    wb += align16(sizeof(float) * kXRows * sp.T);
+    wb += align16(sizeof(float) * 2 * kXRows * sp.T);
     w.pos = (int*)wb;
   } else {
     w.top = (int*)wb;
@@ -199,6 +200,7 @@ __device__ __forceinline__ float vmax(const float (&s)[N]) {
 
 struct XState {
   const float* cj;  // [T][kXRows]: rows 0..U-1 = free positions, row U = -inf padding
+  const float* sf;  // [T][kXRows]: suffix maxima of cj over rows
   const int* pos;   // [U]
   int U, W;
   float thr, rm, two_delta;
@@ -254,6 +256,19 @@ __device__ __forceinline__ void xleaf(XState& x, int (&r)[4], const float (&Sp)[
 #pragma unroll
   for (int p = 0; p < fact_c(C); ++p)
     M[perm_elem_c(C, p, C - 1)] = fmaxf(M[perm_elem_c(C, p, C - 1)], Sp[p]);
+  {
+    // The leaf's best fp32 score, exactly: rounding is monotone, so
+    // max_{rr >= r_lo} fl(M[c] + cj[t_c][rr]) = fl(M[c] + sf[t_c][r_lo]).  It is the score of
+    // a valid action, hence a valid running maximum; if it misses the filter threshold no
+    // action of the leaf can be the argmax and the rows need not be scanned.
+    float sb[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) sb[k] = M[k] + x.sf[x.t[k] * kXRows + r_lo];
+    const float lm = vmax<C>(sb);
+    x.rm = fmaxf(x.rm, lm);
+    x.thr = x.rm - x.two_delta;
+    if (lm < x.thr) return;
+  }
   const float* q[C];
 #pragma unroll
   for (int k = 0; k < C; ++k) q[k] = x.cj + x.t[k] * kXRows + r_lo;
@@ -341,6 +356,16 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
     amax = fmaxf(amax, fabsf(v));
   }
   for (int t = lane; t < T; t += 32) w.cj[t * kXRows + U] = -INFINITY;  // padding row
+  __syncwarp();
+  float* sf = w.cj + T * kXRows;
+  for (int t = lane; t < T; t += 32) {
+    float run = -INFINITY;
+    sf[t * kXRows + U] = run;
+    for (int rr = U - 1; rr >= 0; --rr) {
+      run = fmaxf(run, w.cj[t * kXRows + rr]);
+      sf[t * kXRows + rr] = run;
+    }
+  }
   float lmax = 0.f;
   for (int l = lane; l < L; l += 32) lmax = fmaxf(lmax, fabsf(z[1 + l] - meanL));
   amax = warp_maxf(amax);
@@ -349,6 +374,7 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
   const float v = z[0];
   XState x;
   x.cj = w.cj;
+  x.sf = w.cj + T * kXRows;
   x.pos = w.pos;
   x.U = U;
   x.W = W;
