@@ -432,14 +432,21 @@ __global__ void rowsum_kernel(int rows, int cols, const float* __restrict__ hi,
   if (lane == 0) out[w] = s;
 }
 
-// out[i] = sum_z ws[z][i], deterministic
-__global__ void reduce_splits_kernel(int S, int64_t n, const float* __restrict__ ws,
-                                     float* __restrict__ out) {
+// out[i] = sum_z ws[z][i], deterministic.  With db: ws rows are [N1] wide and the last column
+// (the ones-row product = the bias gradient) goes to db, the rest to out [M][N1 - 1].
+__global__ void reduce_splits_kernel(int S, int64_t n, int N1, const float* __restrict__ ws,
+                                     float* __restrict__ out, float* __restrict__ db) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
     for (int z = 0; z < S; ++z) s += ws[(size_t)z * n + i];
-    out[i] = s;
+    if (db == nullptr) {
+      out[i] = s;
+    } else {
+      const int64_t r = i / N1, c = i - r * N1;
+      if (c == N1 - 1) db[r] = s;
+      else out[r * (N1 - 1) + c] = s;
+    }
   }
 }
 
@@ -566,7 +573,7 @@ hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K,
 }
 
 hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes A, Planes B,
-                         float* ws, size_t ws_elems, float* D) {
+                         float* ws, size_t ws_elems, float* D, float* db) {
   // D[M][N] = A[M][K] . B[N][K]^T, split-K + deterministic reduce
   const long tiles = (long)((M + BM - 1) / BM) * ((N + 127) / 128);
   int S = (int)std::max(1L, std::min(32L, (2L * g->nsm + tiles - 1) / tiles));
@@ -577,12 +584,13 @@ hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes
   TcArgs a{};
   a.M = M; a.N = N; a.K = K; a.kc = kc;
   a.lda = K; a.ldb = K;
-  a.D = S > 1 ? ws : D; a.ldd = N;
+  a.D = (S > 1 || db) ? ws : D; a.ldd = N;
   g->launches++;
   hrp_status s = launch<128, 3, TC_EPI_STORE>(st, A, B, a, S);
-  if (s || S == 1) return s;
+  if (s || (S == 1 && !db)) return s;
   const int64_t n = (int64_t)M * N;
-  reduce_splits_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(S, n, ws, D);
+  reduce_splits_kernel<<<(int)std::min<int64_t>(4 * g->nsm, (n + 255) / 256), 256, 0, st>>>(
+      S, n, N, ws, D, db);
   g->launches++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }

@@ -57,6 +57,16 @@ hrp_status fail(hrp_status s, const std::string& msg) {
 
 bool g_const_ready[64] = {false};
 
+__global__ void fill_ones_kernel(float* p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 1.0f;
+}
+cudaError_t fill_ones(float* p, int64_t n, cudaStream_t st) {
+  fill_ones_kernel<<<(int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, st>>>(p, n);
+  return cudaGetLastError();
+}
+
 hrp_status init_constants(int device) {
   if (device >= 0 && device < 64 && g_const_ready[device]) return HRP_OK;
   int64_t b[65][5];
@@ -488,17 +498,12 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
     const Pl HinT = (i == 0) ? c->XT : c->actT[i - 1];
     float* gW = c->grad + c->woff[i];
     float* gb = gW + (int64_t)fi * fo;
-    // weight and bias gradients (side stream): dW [fo][fi] = dY^T . Hin = dYT . HinT^T over the
-    // Bp (zero-padded) batch columns
+    // weight and bias gradients (side stream): [dW | db] [fo][fi + 1] = dY^T . [Hin | 1] =
+    // dYT . [HinT; ones]^T over the Bp (zero-padded) batch columns -- HinT carries a ones row
     auto wgrad = [&]() -> hrp_status {
       prof_begin(c);
-      hrp_status t = tc_gemm_wgrad(c->tc, c->stream, fo, fi, Bp, dYT.c(), HinT.c(), c->ws_splitk,
-                                   c->ws_splitk_elems, gW);
-      if (t) return fail(t, tc_gemm_error());
-      c->launches += tc_gemm_launches(c->tc) - 1;
-      if ((t = launch_check(c, HRP_K_GEMM_BWD))) return t;
-      prof_begin(c);
-      t = tc_rowsum(c->tc, c->stream, fo, Bp, dYT.c(), gb);
+      hrp_status t = tc_gemm_wgrad(c->tc, c->stream, fo, fi + 1, Bp, dYT.c(), HinT.c(), c->ws_splitk,
+                                   c->ws_splitk_elems, gW, gb);
       if (t) return fail(t, tc_gemm_error());
       c->launches += tc_gemm_launches(c->tc) - 1;
       return launch_check(c, HRP_K_GEMM_BWD);
@@ -741,7 +746,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->grad, sizeof(float) * o));
   size_t ws = 0;
   for (size_t i = 0; i + 1 < c->dims.size(); ++i)
-    ws = std::max(ws, (size_t)32 * c->dims[i] * c->dims[i + 1]);
+    ws = std::max(ws, (size_t)32 * (c->dims[i] + 1) * c->dims[i + 1]);
   c->ws_splitk_elems = ws;
   CK(ar.alloc((void**)&c->ws_splitk, sizeof(float) * ws));
   CK(ar.alloc((void**)&c->win, (size_t)E * W));
@@ -775,21 +780,29 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   c->act_t.resize(cfg->hidden_layers);
   for (auto& p : c->act_t) CK(alloc_pl(p, (size_t)B * wd, split));
   if (split) {
-    // transposed operands: zero padding columns [B, Bp) are never written
-    CK(alloc_pl(c->XT, Bp * in, true));
+    // transposed operands: zero padding columns [B, Bp) are never written.  X^T and the hidden
+    // outputs^T carry one extra row of ones (hi 1, lo 0): the weight-gradient GEMM's product
+    // with it is the bias gradient.
+    auto ones_row = [&](Pl& p, size_t rows) -> cudaError_t {
+      cudaError_t e = cudaMemsetAsync(p.hi, 0, sizeof(float) * Bp * (rows + 1), c->stream);
+      if (e == cudaSuccess) e = cudaMemsetAsync(p.lo, 0, sizeof(float) * Bp * (rows + 1), c->stream);
+      if (e == cudaSuccess) e = fill_ones(p.hi + Bp * rows, Bp, c->stream);
+      return e;
+    };
+    CK(alloc_pl(c->XT, Bp * (in + 1), true));
     CK(alloc_pl(c->dzT, Bp * H, true));
-    CK(cudaMemsetAsync(c->XT.hi, 0, sizeof(float) * Bp * in, c->stream));
-    CK(cudaMemsetAsync(c->XT.lo, 0, sizeof(float) * Bp * in, c->stream));
+    CK(ones_row(c->XT, in));
     CK(cudaMemsetAsync(c->dzT.hi, 0, sizeof(float) * Bp * H, c->stream));
     CK(cudaMemsetAsync(c->dzT.lo, 0, sizeof(float) * Bp * H, c->stream));
     c->actT.resize(cfg->hidden_layers);
     c->dhs.resize(cfg->hidden_layers);
     c->dhTs.resize(cfg->hidden_layers);
     for (int i = 0; i < cfg->hidden_layers; ++i) {
-      CK(alloc_pl(c->actT[i], Bp * wd, true));
+      CK(alloc_pl(c->actT[i], Bp * (wd + 1), true));
       CK(alloc_pl(c->dhs[i], (size_t)B * wd, true));
       CK(alloc_pl(c->dhTs[i], Bp * wd, true));
-      for (float* q : {c->actT[i].hi, c->actT[i].lo, c->dhTs[i].hi, c->dhTs[i].lo})
+      CK(ones_row(c->actT[i], wd));
+      for (float* q : {c->dhTs[i].hi, c->dhTs[i].lo})
         CK(cudaMemsetAsync(q, 0, sizeof(float) * Bp * wd, c->stream));
     }
   }
@@ -1082,11 +1095,20 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
         b8v[nb8++] = b;
       }
     }
+  int n_items = 0;
   {
     int64_t tmax = 0;
     for (int i = 0; i < prof->n_jobs; ++i) tmax = std::max<int64_t>(tmax, prof->solo_ticks[i]);
-    // memory term <= Tmax * Cmax * 1000 * (8 + q (Cmax - 1)) / 1000 (demand <= 1000 permille)
-    const double bound = (double)tmax * hs.cmax * (8.0 + (double)space->interference_q3 * (hs.cmax - 1));
+    // memory term <= Tmax * Cmax * 1000 * (8 + q (Cmax - 1)) / 1000 (demand <= 1000 permille);
+    // compute term <= Tmax * 4 * 1000 / (5 * min sm800); Solo <= Cmax * Tmax.  The kernel keeps
+    // all of them in 32 bits.
+    int min_sm = 800;
+    for (int l = 0; l < hs.L; ++l) {
+      n_items += fact_c(hs.nslots[l]);
+      for (int k = 0; k < hs.nslots[l]; ++k) min_sm = std::min<int>(min_sm, hs.slots[l][k].sm800);
+    }
+    const double bound = std::max((double)tmax * hs.cmax * (8.0 + (double)space->interference_q3 * (hs.cmax - 1)),
+                                  (double)tmax * 4000.0 / (5.0 * std::max(1, min_sm)) + 1.0);
     if (bound >= 4294967296.0) return fail(HRP_ERANGE, "brute force: solo ticks too large");
   }
   if (n == 0) return HRP_OK;
@@ -1097,7 +1119,8 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   Arena ar;
   DevTables dt;
   if ((s = upload_tables(hs, prof, true, ar, st, dt))) { ar.release(); return s; }
-  const size_t smem = brute_smem_bytes(hs.W, hs.L, hs.T);
+  const size_t smem = brute_smem_bytes(hs.W, hs.T, n_items);
+  if (smem > 227 * 1024) { ar.release(); return fail(HRP_ERANGE, "brute force: layout space too large for shared memory"); }
   static int brute_smem_max[64] = {0};
   cudaError_t e = cudaSuccess;
   if ((int)smem > brute_smem_max[dev & 63]) {
@@ -1107,10 +1130,11 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   if (e != cudaSuccess) { ar.release(); return fail(HRP_ECUDA, cudaGetErrorString(e)); }
   int nsm = 148, occ = 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brute_kernel, 512, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brute_kernel, kBruteThreads, smem);
   const int grid = (int)std::min<int64_t>(n, (int64_t)nsm * std::max(1, occ));
-  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact, nb8, {b8v[0], b8v[1], b8v[2], b8v[3]}};
-  brute_kernel<<<grid, 512, smem, st>>>(dt.sp, dt.pool, a);
+  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact, nb8, {b8v[0], b8v[1], b8v[2], b8v[3]},
+               n_items};
+  brute_kernel<<<grid, kBruteThreads, smem, st>>>(dt.sp, dt.pool, a);
   e = cudaGetLastError();
   cudaError_t e2 = cudaStreamSynchronize(st);
   ar.release();
