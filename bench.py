@@ -217,12 +217,30 @@ def run_gpu(args, cfg):
         ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         n_launch0 = sess.launches()
         evals0 = hrp.hrp_eval_counts(sess.ctx)
+        graphs = []
+        if args.graph:
+            # one CUDA graph per timed step (each step's inputs live at their own addresses and
+            # the context's host counters -- step t, replay fill -- advance as the launches are
+            # recorded), replayed once each, in capture order
+            for k in range(args.steps):
+                t = args.warmup + k
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    one_step(t, streams_d[t])
+                graphs.append(g)
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
         clocks = Clocks(local)
         for k in range(args.steps):
             t = args.warmup + k
             flush.zero_()                       # L2 flushed between timed steps
             ev0[k].record(stream)
-            one_step(t, streams_d[t])
+            if args.graph:
+                graphs[k].replay()
+            else:
+                one_step(t, streams_d[t])
             ev1[k].record(stream)
         stream.synchronize()
         clk = clocks.stop()
@@ -266,16 +284,34 @@ def run_gpu(args, cfg):
         torch.cuda.synchronize(dev)
         f0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         f1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-        for k in range(args.steps):
+
+        def e2e_step(k):
             t = args.warmup + k
-            flush.zero_()                       # L2 flushed between timed steps, as above
-            f0[k].record(stream)
             for key, v in pinned[k].items():
                 bufs[key].copy_(v, non_blocking=True)
             one_step(t, bufs)
             out_h["actions"].copy_(sess.actions, non_blocking=True)
             out_h["rewards"].copy_(sess.rewards, non_blocking=True)
             out_h["loss"].copy_(sess.loss, non_blocking=True)
+
+        graphs_e2e = []
+        if args.graph:
+            for k in range(args.steps):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    e2e_step(k)
+                graphs_e2e.append(g)
+            stream.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+        for k in range(args.steps):
+            flush.zero_()                       # L2 flushed between timed steps, as above
+            f0[k].record(stream)
+            if args.graph:
+                graphs_e2e[k].replay()          # H2D copies, step, D2H copies
+            else:
+                e2e_step(k)
             f1[k].record(stream)
         stream.synchronize()
         ms_e2e = sum(a.elapsed_time(b) for a, b in zip(f0, f1))
@@ -291,6 +327,8 @@ def run_gpu(args, cfg):
                           "argmax": "explicit" if sess_explicit(args, sc) else "pruned-exact",
                           "gemm": {0: "auto", 1: "fp32 CUDA-core", 2: "tcgen05 3xTF32"}[args.gemm],
                           "l2": "flushed (256 MiB memset) between timed steps",
+                          "launch": "CUDA graph per step (captured before the timed region)"
+                                    if args.graph else "eager stream launches",
                           "parallelism": f"dp{world} (env sharding + NCCL grad allreduce)"},
                "q_evals_per_s": evals * world / (ms / 1e3),
                "q_evals_per_step": evals / args.steps,
@@ -461,7 +499,9 @@ def run_brute(args, cfg):
     from math import comb, factorial
     nc = np.bincount(np.asarray(tab["nslots"]), minlength=5)
     evals = sum(comb(W, c) * int(nc[c]) * factorial(c) for c in range(1, 5))
-    slot_terms = sum(comb(W, c) * int(nc[c]) * factorial(c) * c for c in range(1, 5))
+    # per evaluation: CoRun = max over 2C terms (C compute terms, C memory terms), one lane-op
+    # each (the (CoRun, idx) minimum update folds into the last one)
+    slot_terms = sum(comb(W, c) * int(nc[c]) * factorial(c) * 2 * c for c in range(1, 5))
     sec = ms / 1e3
     value = n * args.steps / sec
     pk = _peaks()
@@ -484,9 +524,8 @@ def run_brute(args, cfg):
            "roofline": {"kernel": "brute_kernel", "bound": "alu", "achieved": ach,
                         "peak": alu_peak, "unit": "Tops/s", "frac": ach / alu_peak,
                         "traffic": None,
-                        "work": f"{slot_terms} slot terms per window (one lane-op each, a lower "
-                                f"bound on the integer work of {evals} (set, layout, sigma) "
-                                f"evaluations)",
+                        "work": f"{slot_terms} CoRun terms per window (2C per (set, layout, "
+                                f"sigma) evaluation, one lane-op each; {evals} evaluations)",
                         "peak_src": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)"}}
     if not args.no_cpu_baseline:
         from oracle import brute as BR
@@ -599,6 +638,8 @@ def main():
     ap.add_argument("--argmax", type=int, default=0, help="0 auto, 1 explicit, 2 pruned")
     ap.add_argument("--gemm", type=int, default=0, help="0 auto, 1 CUDA-core fp32, 2 tcgen05")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the timed steps eagerly instead of from per-step CUDA graphs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -1,20 +1,22 @@
 // a14: exhaustive optimum of the co-scheduling problem (baselines P:246-248).
 //
 // One CTA per window (grid-stride), W <= 12, everything in shared memory:
-//  setup    (once per CTA) the (layout, permutation) item table of the layout space: for every
-//           slot count C, every layout l with C slots (index order) and every member->slot
-//           permutation sigma (Lehmer order) one entry holding, per member i, the slot type of
-//           slot sigma(i), the members sharing sigma(i)'s memory domain (a 4-bit member mask)
-//           and that domain's memory-size index, plus off[l] + lehmer(sigma).  Everything in a
-//           (set, l, sigma) evaluation that does not depend on the job set.
+//  setup    (once per CTA) the layout tables of the space, grouped by slot count C (layout index
+//           order within a group): per layout its packed slot types and off[l]; per (layout,
+//           member->slot permutation sigma in Lehmer order) one word whose byte i is the
+//           memory-term table entry of member i: (memory-size index of slot sigma(i), members
+//           sharing sigma(i)'s memory domain as a 4-bit mask).  Everything in a (set, l, sigma)
+//           evaluation that does not depend on the job set.
 //  phase 1  best(B) for every job set B (|B| <= Cmax): one warp per set.  The warp first builds
 //           the set's memory-term table memw[b8][member mask] (R8: ceil(max_k T_k X / Y),
 //           X = max(Y, D (8 + q (n - 1))), Y = 1000 b8, D = sum of the members' memory demand;
-//           max_k ceil(T_k X/Y) = ceil(max_k T_k X/Y) because ceil is monotone), then its lanes
-//           stride over the item table: CoRun = max over members of the compute term
-//           tc[job][slot type] and memw[...] -- 2C shared-memory lookups and no atomics.
-//           Feasible iff CoRun <= Solo(B); the min over (CoRun, action index) is a packed key
-//           (CoRun << 26 | idx), warp-reduced and stored once.
+//           max_k ceil(T_k X/Y) = ceil(max_k T_k X/Y) because ceil is monotone).  Then lane <->
+//           layout: the lane loads the C x C compute terms Mc[i][s] = tc[job i][type of slot s]
+//           into registers once and walks the C! permutations unrolled at compile time, so a
+//           (set, l, sigma) evaluation is C register maxes for the compute term plus C memw
+//           lookups -- no atomics.  Feasible iff CoRun <= Solo(B); the lowest (CoRun, action
+//           index) is kept per lane (ascending index order, strict <), then warp-reduced as a
+//           packed key (CoRun << 26 | idx) and stored once.
 //  phase 2  subset DP over the 2^W sets, level by level in popcount order:
 //           OPT(S) = min over B containing min(S) of best(B) + OPT(S \ B), ties broken by the
 //           block-order rule (prefer the block whose W-bit reversal is larger, reading R21b).
@@ -42,21 +44,27 @@ struct BruteArgs {
   int n_items;          // sum over layouts of (slots)!
 };
 
+// memory-term table entry of member i under permutation word mi, as a byte offset into memw
+__device__ __forceinline__ uint32_t memw_at(const uint32_t* memw, uint32_t mi, int i) {
+  return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint8_t*>(memw) +
+                                            ((mi >> (8 * i)) & 255));
+}
+
 __device__ __forceinline__ uint32_t bitrev_w(uint32_t m, int W) { return __brev(m) >> (32 - W); }
 
 __host__ __device__ inline size_t brute_smem_bytes(int W, int T, int n_items) {
   const size_t S = size_t(1) << W;
-  return S * 8 /*bestkey*/ + S * 8 /*dp*/ + (size_t)n_items * 12 /*items*/ +
+  return S * 8 /*bestkey*/ + S * 8 /*dp*/ + (size_t)n_items * 4 + 512 * 8 /*layout tables*/ +
          (size_t)(kBruteThreads / 32) * 64 * 4 /*memw*/ + (size_t)W * T * 4 /*tc*/ +
          S * 2 /*choice*/ + 64;
 }
 
-// One job set (members packed in memb, lex rank r among the C-sets) by one warp.
+// One job set (members packed in memb, lex rank r among the C-sets) by one warp; lane <-> layout.
 template <int C>
-__device__ __forceinline__ void brute_set(int lane, uint32_t memb, int r, int n_it,
-                                          const uint32_t* __restrict__ ity,
-                                          const uint32_t* __restrict__ idm,
-                                          const uint32_t* __restrict__ iof,
+__device__ __forceinline__ void brute_set(int lane, uint32_t memb, int r, int nl,
+                                          const uint32_t* __restrict__ lty,
+                                          const uint32_t* __restrict__ loff,
+                                          const uint32_t* __restrict__ lmi,
                                           const uint32_t* __restrict__ tcw, int T,
                                           uint32_t* memw, const int64_t* Tw, const int64_t* mw,
                                           const BruteArgs& a, int q3,
@@ -92,22 +100,33 @@ __device__ __forceinline__ void brute_set(int lane, uint32_t memb, int r, int n_
     memw[e] = v;
   }
   __syncwarp();
-  unsigned long long best = ~0ull;
-  const uint32_t rF = (uint32_t)r * F;
-  for (int t = lane; t < n_it; t += 32) {
-    const uint32_t ty = ity[t], dm = idm[t];
-    uint32_t cr = 0;
+  // running best per lane: CoRun < bcr (strict, ascending index order keeps the lowest index);
+  // bcr starts at Solo + 1, so the first accepted evaluation is a feasible one
+  uint32_t bcr = solo + 1, bidx = 0;
+  for (int li = lane; li < nl; li += 32) {
+    const uint32_t ty = lty[li], of = loff[li];
+    const uint32_t* mrow = lmi + li * F;
+    uint32_t Mc[C][C];
 #pragma unroll
-    for (int i = 0; i < C; ++i) {
-      cr = max(cr, tcw[gT[i] + ((ty >> (8 * i)) & 255)]);
-      cr = max(cr, memw[(((dm >> (16 + 2 * i)) & 3) << 4) | ((dm >> (4 * i)) & 15)]);
+    for (int s = 0; s < C; ++s) {
+      const int tau = (ty >> (8 * s)) & 255;
+#pragma unroll
+      for (int i = 0; i < C; ++i) Mc[i][s] = tcw[gT[i] + tau];
     }
-    if (cr <= solo) {
-      const unsigned long long key =
-          ((unsigned long long)cr << kBruteIdxBits) | (unsigned long long)(iof[t] + rF);
-      best = key < best ? key : best;
+#pragma unroll
+    for (int pp = 0; pp < F; ++pp) {
+      const uint32_t mi = mrow[pp];
+      uint32_t cr = Mc[0][perm_elem_c(C, pp, 0)];
+#pragma unroll
+      for (int i = 1; i < C; ++i) cr = max(cr, Mc[i][perm_elem_c(C, pp, i)]);
+#pragma unroll
+      for (int i = 0; i < C; ++i) cr = max(cr, memw_at(memw, mi, i));
+      if (cr < bcr) { bcr = cr; bidx = of + pp; }
     }
   }
+  unsigned long long best = bcr <= solo
+      ? ((unsigned long long)bcr << kBruteIdxBits) | (unsigned long long)(bidx + (uint32_t)r * F)
+      : ~0ull;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, best, o);
@@ -125,9 +144,9 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
   uint8_t* p = smem_raw;
   unsigned long long* bestkey = (unsigned long long*)p; p += S * 8;
   int64_t* dp = (int64_t*)p; p += S * 8;
-  uint32_t* ity = (uint32_t*)p; p += a.n_items * 4;
-  uint32_t* idm = (uint32_t*)p; p += a.n_items * 4;
-  uint32_t* iof = (uint32_t*)p; p += a.n_items * 4;
+  uint32_t* lmi = (uint32_t*)p; p += a.n_items * 4;
+  uint32_t* lty = (uint32_t*)p; p += 512 * 4;
+  uint32_t* loff = (uint32_t*)p; p += 512 * 4;
   uint32_t* memw_all = (uint32_t*)p; p += nwarp * 64 * 4;
   uint32_t* tcw = (uint32_t*)p; p += W * T * 4;
   uint16_t* choice = (uint16_t*)p; p += S * 2;
@@ -149,12 +168,16 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
     ibase[5] = it;
   }
   __syncthreads();
+  for (int k = threadIdx.x; k < ilay[5]; k += blockDim.x) {
+    const int l = lay_of_c[k];
+    lty[k] = sp.lay_stype[l];
+    loff[k] = (uint32_t)sp.off[l];
+  }
   for (int C = 1; C <= 4; ++C) {
     const int F = fact_c(C), n = ibase[C + 1] - ibase[C];
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
       const int li = t / F, pp = t - li * F;
       const int l = lay_of_c[ilay[C] + li];
-      const uint32_t st = sp.lay_stype[l];
       int sl[4], dom[4], bi[4];
       for (int s = 0; s < C; ++s) {
         const uint32_t v = sp.lay_slot[l * 4 + s];
@@ -164,17 +187,13 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
           if ((int)((v >> 16) & 255) == a.b8v[q]) bi[s] = q;
       }
       for (int i = 0; i < C; ++i) sl[i] = perm_elem_c(C, pp, i);
-      uint32_t ty = 0, dm = 0;
+      uint32_t mi = 0;
       for (int i = 0; i < C; ++i) {
-        ty |= ((st >> (8 * sl[i])) & 255) << (8 * i);
         uint32_t mm = 0;
         for (int i2 = 0; i2 < C; ++i2) mm |= (dom[sl[i2]] == dom[sl[i]]) ? 1u << i2 : 0u;
-        dm |= mm << (4 * i);
-        dm |= (uint32_t)bi[sl[i]] << (16 + 2 * i);
+        mi |= ((uint32_t)(bi[sl[i]] * 16 + mm) * 4) << (8 * i);   // byte offset into memw
       }
-      ity[ibase[C] + t] = ty;
-      idm[ibase[C] + t] = dm;
-      iof[ibase[C] + t] = (uint32_t)(sp.off[l] + pp);
+      lmi[ibase[C] + t] = mi;
     }
   }
   __syncthreads();
@@ -196,20 +215,20 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
       int k = 0;
       for (int C = 1; C <= sp.cmax; ++C) {
         const int nb = sp.ncombo[C];
-        const int n_it = ibase[C + 1] - ibase[C];
+        const int nl = ilay[C + 1] - ilay[C];
         const uint32_t* combo = sp.combo[C];
         const int first = ((warp - k) % nwarp + nwarp) % nwarp;
         for (int r = first; r < nb; r += nwarp) {
           const uint32_t memb = combo[r];
-          const int b0 = ibase[C];
+          const int b0 = ibase[C], l0 = ilay[C];
           if (C == 1)
-            brute_set<1>(lane, memb, r, n_it, ity + b0, idm + b0, iof + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
+            brute_set<1>(lane, memb, r, nl, lty + l0, loff + l0, lmi + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
           else if (C == 2)
-            brute_set<2>(lane, memb, r, n_it, ity + b0, idm + b0, iof + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
+            brute_set<2>(lane, memb, r, nl, lty + l0, loff + l0, lmi + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
           else if (C == 3)
-            brute_set<3>(lane, memb, r, n_it, ity + b0, idm + b0, iof + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
+            brute_set<3>(lane, memb, r, nl, lty + l0, loff + l0, lmi + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
           else
-            brute_set<4>(lane, memb, r, n_it, ity + b0, idm + b0, iof + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
+            brute_set<4>(lane, memb, r, nl, lty + l0, loff + l0, lmi + b0, tcw, T, memw, Tw, mw, a, sp.q3, bestkey);
         }
         k += nb;
       }

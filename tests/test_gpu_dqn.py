@@ -136,3 +136,52 @@ def test_config2_full_size_step_sampled():
     np.testing.assert_array_equal(sess.corun.cpu().numpy()[pick], cr)
     close(sess.rewards.cpu().numpy()[pick], r, what="rewards")
     close(sess.qsel.cpu().numpy()[pick], q, what="qsel")
+
+
+def test_cuda_graph_replay_equals_eager():
+    # bench.py times per-step CUDA graphs: steps recorded into graphs (host counters advancing
+    # at capture) and replayed in order must reproduce eager launches bit for bit, on two
+    # streams (fork/join events) and the tensor-core path
+    from paper_2405_08754_b200.session import Session, streams_to_dev
+    cfg = synth.config(2)
+    pool = synth.make_pool(27)
+    osp = SP.build_space(16, 3, cfg.space.shares)
+    th = synth.init_weights(QN.net_dims(osp, cfg.net))
+    E = B = 256
+    outs = []
+    for use_graph in (False, True):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sess = Session(cfg, pool, n_envs=E, batch=B, init_weights=th, replay=4096,
+                           stream=stream)
+            sess.reset(synth.make_windows(pool, E, 16))
+            steps = [streams_to_dev(synth.step_streams(t, E, B, 16, pool), sess.dev)
+                     for t in range(6)]
+            rec, graphs = [], []
+            for t, d in enumerate(steps):
+                thr = synth.eps_threshold(t, cfg.n_decay)
+
+                def one(t=t, d=d, thr=thr):
+                    sess.step(thr, d["u_explore"], d["u_action"], d["next_windows"], extras=False)
+                    sess.update(d["u_replay"], t % 3 == 2, extras=False)
+                if use_graph and t >= 2:
+                    # as bench.py: capture every remaining step first, then replay in order
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        one()
+                    graphs.append(g)
+                    continue
+                one()
+                stream.synchronize()
+                rec.append((sess.actions.clone(), sess.rewards.clone(), sess.loss.clone()))
+            for g in graphs:
+                g.replay()
+                stream.synchronize()
+                rec.append((sess.actions.clone(), sess.rewards.clone(), sess.loss.clone()))
+            rec.append(torch.from_numpy(sess.weights()))
+            outs.append(rec)
+            sess.close()
+    for x, y in zip(outs[0][:-1], outs[1][:-1]):
+        for u, v in zip(x, y):
+            assert torch.equal(u, v)
+    assert torch.equal(outs[0][-1], outs[1][-1])
