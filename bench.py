@@ -424,12 +424,23 @@ def rooflines(prof, steps, evals, cfg, osp):
     return out
 
 
+def measured_traffic(cls):
+    """DRAM bytes per launch of kernel class `cls` from the committed ncu launch list of this
+    bench command (profiles/traffic.json, written by tools/traffic_from_launches.py), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return t["classes"][cls]["dram_bytes_per_launch"], t["source"]
+    except Exception:
+        return None, None
+
+
 def dominant(rl):
     name = max(rl, key=lambda k: rl[k]["ms_per_step"])
     r = rl[name]
+    traffic, src = measured_traffic(name)
     return {"kernel": name, "bound": r.get("bound"), "achieved": r.get("achieved"),
             "peak": r.get("peak"), "unit": r.get("unit"), "frac": r.get("frac"),
-            "traffic": None, "peak_src": r.get("peak_src"),
+            "traffic": traffic, "traffic_src": src, "peak_src": r.get("peak_src"),
             "share_of_step": None}
 
 
@@ -523,7 +534,7 @@ def run_brute(args, cfg):
            "clocks": clk,
            "roofline": {"kernel": "brute_kernel", "bound": "alu", "achieved": ach,
                         "peak": alu_peak, "unit": "Tops/s", "frac": ach / alu_peak,
-                        "traffic": None,
+                        "traffic": measured_traffic("brute")[0],
                         "work": f"{slot_terms} CoRun terms per window (2C per (set, layout, "
                                 f"sigma) evaluation, one lane-op each; {evals} evaluations)",
                         "peak_src": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)"}}

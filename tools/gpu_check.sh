@@ -1,6 +1,6 @@
 #!/bin/bash
-# One gpurun call: GPU parity tests, the bench line, the ncu launch list and full captures.
-# usage: tools/gpu_check.sh TAG [full-capture kernel regexes...]
+# One gpurun call: GPU parity tests, the bench line, the ncu launch list (time + DRAM bytes per
+# launch) and full captures.  usage: tools/gpu_check.sh TAG [full-capture kernel regexes...]
 set -x
 TAG=${1:-v}; shift
 mkdir -p gpurun_out
@@ -8,7 +8,8 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  --clock-control none -c 600 --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline \
   > gpurun_out/${TAG}_ncu_bench.log 2>&1
 for K in "$@"; do
