@@ -655,6 +655,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # per-step graphs are verified on one GPU only (tests/test_gpu_dqn.py); with NCCL inside
+        # the step the multi-rank run launches eagerly
+        args.graph = False
     cfg = synth.config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)

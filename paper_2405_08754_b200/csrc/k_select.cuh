@@ -558,14 +558,46 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   const int64_t Fv = fixed_point(z[0]);
   best = INT64_MIN;
   bidx = INT64_MAX;
-  for (int l = lane; l < sp.L; l += 32) {
+  // Seed: per layout the first leaf of its search (slot k takes its best Top-list job not
+  // already taken) -- a valid action, so (best, bidx) may start at the warp's best seed; the
+  // bound then prunes most layouts at the first level.
+  for (int i = lane; i < sp.L; i += 32) {
+    const int l = tb.lay_of_c[i];
     const int C = tb.nsl[l];
     const uint32_t ty = tb.stype[l];
-    const int64_t base = Fv + fixed_point(z[1 + l] - meanL);
-    if (C == 1) psearch<1>(tb, w, l, W, ty, base, best, bidx, nevals);
-    else if (C == 2) psearch<2>(tb, w, l, W, ty, base, best, bidx, nevals);
-    else if (C == 3) psearch<3>(tb, w, l, W, ty, base, best, bidx, nevals);
-    else psearch<4>(tb, w, l, W, ty, base, best, bidx, nevals);
+    int js[4] = {0, 0, 0, 0};
+    int64_t v = Fv + fixed_point(z[1 + l] - meanL);
+    bool ok = true;
+    for (int k = 0; k < C && ok; ++k) {
+      const int t = (ty >> (8 * k)) & 255;
+      ok = false;
+      for (int q = 0; q < 4; ++q) {
+        const int j = w.top[t * 4 + q];
+        if (j < 0) break;
+        bool used = false;
+        for (int k2 = 0; k2 < k; ++k2) used |= js[k2] == j;
+        if (!used) { js[k] = j; v += w.topv[t * 4 + q]; ok = true; break; }
+      }
+    }
+    if (!ok || v < best) continue;
+    if (C == 1) pleaf<1>(tb, l, W, js, v, best, bidx);
+    else if (C == 2) pleaf<2>(tb, l, W, js, v, best, bidx);
+    else if (C == 3) pleaf<3>(tb, l, W, js, v, best, bidx);
+    else pleaf<4>(tb, l, W, js, v, best, bidx);
+  }
+  warp_best(best, bidx);
+  // Exhaustive pruned search, lanes over layouts grouped by slot count (C-uniform rounds).
+#pragma unroll 1
+  for (int C = 1; C <= 4; ++C) {
+    for (int i = tb.cstart[C] + lane; i < tb.cstart[C + 1]; i += 32) {
+      const int l = tb.lay_of_c[i];
+      const uint32_t ty = tb.stype[l];
+      const int64_t base = Fv + fixed_point(z[1 + l] - meanL);
+      if (C == 1) psearch<1>(tb, w, l, W, ty, base, best, bidx, nevals);
+      else if (C == 2) psearch<2>(tb, w, l, W, ty, base, best, bidx, nevals);
+      else if (C == 3) psearch<3>(tb, w, l, W, ty, base, best, bidx, nevals);
+      else psearch<4>(tb, w, l, W, ty, base, best, bidx, nevals);
+    }
   }
   warp_best(best, bidx);
 }
