@@ -449,14 +449,21 @@ template <int C>
 __device__ __forceinline__ void pleaf(const PTabs& tb, int l, int W, const int (&js)[4], int64_t v,
                                       int64_t& best, int64_t& bidx) {
   // group g = sorted jobs; sigma(i) = slot of member g_i; index = off + rank(g) C! + lehmer
-  int g[4], sg[4];
+  int g[4], sg[4], rk_[4];
 #pragma unroll
   for (int i = 0; i < C; ++i) {
     int r = 0;
 #pragma unroll
     for (int i2 = 0; i2 < C; ++i2) r += js[i2] < js[i];
-    g[r] = js[i];
-    sg[r] = i;
+    rk_[i] = r;
+  }
+#pragma unroll
+  for (int k = 0; k < C; ++k) {          // g[k] = the member of rank k (selects, no local memory)
+    g[k] = 0;
+    sg[k] = 0;
+#pragma unroll
+    for (int i = 0; i < C; ++i)
+      if (rk_[i] == k) { g[k] = js[i]; sg[k] = i; }
   }
   int64_t rk = 0;
   int prev = -1;
@@ -538,19 +545,24 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   const int W = sp.W, T = sp.T;
   const float* aJ = z + 1 + sp.L;
   for (int t = lane; t < T; t += 32) {
-    // top-4 by (value desc, position asc): register-only insertion network
+    // top-4 by (value desc, position asc): register-only insertion network.  x < x3 (fp32)
+    // implies F(x) <= F(x3) = b3 (F is monotone), so most positions are rejected before the
+    // fixed-point conversion; the exact test is still on F.
     int64_t b0 = INT64_MIN, b1 = INT64_MIN, b2 = INT64_MIN, b3 = INT64_MIN;
+    float x0 = -INFINITY, x1 = -INFINITY, x2 = -INFINITY, x3 = -INFINITY;
     int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
     const float mj = w.meanJ[t];
     for (int j = 0; j < W; ++j) {
-      if ((sched >> j) & 1ull) continue;
-      const int64_t v = fixed_point(aJ[j * T + t] - mj);
+      const float x = aJ[j * T + t] - mj;
+      if (x < x3 || ((sched >> j) & 1ull)) continue;
+      const int64_t v = fixed_point(x);
       if (v <= b3) continue;  // ties keep the lower position
-      b3 = v; j3 = j;
-      if (b3 > b2) { int64_t x = b2; b2 = b3; b3 = x; int y = j2; j2 = j3; j3 = y; }
-      if (b2 > b1) { int64_t x = b1; b1 = b2; b2 = x; int y = j1; j1 = j2; j2 = y; }
-      if (b1 > b0) { int64_t x = b0; b0 = b1; b1 = x; int y = j0; j0 = j1; j1 = y; }
+      b3 = v; j3 = j; x3 = x;
+      if (b3 > b2) { int64_t u = b2; b2 = b3; b3 = u; int y = j2; j2 = j3; j3 = y; float f = x2; x2 = x3; x3 = f; }
+      if (b2 > b1) { int64_t u = b1; b1 = b2; b2 = u; int y = j1; j1 = j2; j2 = y; float f = x1; x1 = x2; x2 = f; }
+      if (b1 > b0) { int64_t u = b0; b0 = b1; b1 = u; int y = j0; j0 = j1; j1 = y; float f = x0; x0 = x1; x1 = f; }
     }
+    (void)x0;
     w.top[t * 4 + 0] = j0; w.top[t * 4 + 1] = j1; w.top[t * 4 + 2] = j2; w.top[t * 4 + 3] = j3;
     w.topv[t * 4 + 0] = b0; w.topv[t * 4 + 1] = b1; w.topv[t * 4 + 2] = b2; w.topv[t * 4 + 3] = b3;
   }
@@ -568,13 +580,17 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
     int js[4] = {0, 0, 0, 0};
     int64_t v = Fv + fixed_point(z[1 + l] - meanL);
     bool ok = true;
-    for (int k = 0; k < C && ok; ++k) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {          // constant indices: js stays in registers
+      if (k >= C || !ok) break;
       const int t = (ty >> (8 * k)) & 255;
       ok = false;
+#pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int j = w.top[t * 4 + q];
         if (j < 0) break;
         bool used = false;
+#pragma unroll
         for (int k2 = 0; k2 < k; ++k2) used |= js[k2] == j;
         if (!used) { js[k] = j; v += w.topv[t * 4 + q]; ok = true; break; }
       }
