@@ -389,6 +389,7 @@ def rooflines(prof, steps, evals, cfg, osp):
     F = sum(2 * dims[i] * dims[i + 1] for i in range(len(dims) - 1))
     E, B = cfg.n_envs, cfg.batch
     out = {}
+    head_struct = prof.get("head_bwd", (0.0, 0))[1] > 0
     for name, (ms, cnt) in prof.items():
         if cnt == 0 or ms <= 0:
             continue
@@ -402,7 +403,15 @@ def rooflines(prof, steps, evals, cfg, osp):
                        peak_src="148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)")
         elif name in ("gemm_fwd", "gemm_bwd"):
             rows = E + 3 * B if name == "gemm_fwd" else B
-            flops = (rows * F if name == "gemm_fwd" else B * (2 * F - 2 * dims[0] * dims[1]))
+            if name == "gemm_fwd":
+                flops = rows * F
+            else:
+                # weight gradients of every GEMM layer + data gradients of all but the first;
+                # with the structured head (class head_bwd) the head layer has no GEMMs
+                nl = len(dims) - 1
+                top = nl - 1 if head_struct else nl
+                flops = sum(2 * B * dims[i] * dims[i + 1] * (2 if i > 0 else 1)
+                            for i in range(top))
             ach = flops * steps / sec / 1e12
             per.update(bound="tensor", achieved=ach, peak=fp32_tc, unit="TFLOP/s",
                        frac=ach / fp32_tc, work=f"{flops / 1e9:.4g} GFLOP/step (logical fp32)",
@@ -411,6 +420,15 @@ def rooflines(prof, steps, evals, cfg, osp):
         elif name == "encode":
             rows = E + 2 * B
             byts = rows * (osp.W * 17 * 4 + osp.W + 8)
+            ach = byts * steps / sec / 1e9
+            per.update(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm,
+                       work=f"{byts / 1e6:.4g} MB/step")
+        elif name == "head_bwd":
+            # structured head backward: per sample the last hidden row h (hi + lo planes) read
+            # twice (gather and scatter), dL/dh written split and transposed (4 planes); the
+            # W_head rows and the fp64 accumulators stay in L2
+            w = dims[-2]
+            byts = B * w * 4 * (4 + 4)
             ach = byts * steps / sec / 1e9
             per.update(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm,
                        work=f"{byts / 1e6:.4g} MB/step")

@@ -196,7 +196,8 @@ typedef enum {
   HRP_K_SGD = 6,      /* a13 SGD + target sync                                        */
   HRP_K_MISC = 7,     /* loss reduction                                             */
   HRP_K_ALLREDUCE = 8,/* a12 NCCL gradient allreduce (world > 1)                      */
-  HRP_K_COUNT = 9
+  HRP_K_HEAD_BWD = 9, /* a10-a11 structured duelling-head backward (gathers / scatters) */
+  HRP_K_COUNT = 10
 } hrp_kernel_class;
 hrp_status hrp_profile(hrp_ctx *ctx, int enable); /* 1: clear + start recording; 0: stop */
 hrp_status hrp_profile_read(hrp_ctx *ctx, double *ms, int64_t *launches);

@@ -18,6 +18,7 @@
 #include "k_env.cuh"
 #include "k_brute.cuh"
 #include "k_select.cuh"
+#include "k_head.cuh"
 #include "gemm_tc.h"
 
 using namespace hrp;
@@ -279,6 +280,12 @@ struct hrp_ctx {
   int Bp = 0;
   Pl XT, dzT;
   std::vector<Pl> actT;
+  // structured head backward (k_head.cuh; tensor-core path): td writes per-sample descriptors
+  // instead of the dense dz, the head's two backward GEMMs become gathers / scatters
+  bool head_struct = false;
+  int* hdesc = nullptr;               // [B][8]
+  double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
+  float *hc0 = nullptr, *hmT = nullptr;      // [w], [T][w]
   uint8_t* bwin = nullptr;            // [2B][W] or [chunk][W]
   uint64_t* bsched = nullptr;
   int64_t* bact = nullptr;
@@ -489,12 +496,60 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
   const int Bp = c->Bp;
   const bool conc = concurrent(c);
   hrp_status s;
-  if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, c->ldz, c->dz, c->dzT, Bp))) return s;
-  if (conc && (s = fork(c))) return s;
   Pl dY = c->dz, dYT = c->dzT;
   int ldy = c->ldz;
-  for (int i = nl - 1; i >= 0; --i) {
-    const int fi = c->dims[i], fo = c->dims[i + 1];
+  int top = nl - 1;
+  if (c->head_struct) {
+    // head layer (nl - 1): dL/dh of the last hidden layer by gathers of W_head rows (main
+    // stream), head weight / bias gradients by fp64 scatter-adds (side stream) -- k_head.cuh
+    const int w = c->dims[nl - 1];
+    HeadArgs h{};
+    h.B = B; h.w = w; h.H = H; h.L = c->hs.L; h.T = c->hs.T; h.W = c->hs.W;
+    h.hdesc = c->hdesc;
+    h.Wh = c->theta + c->woff[nl - 1];
+    h.hh = c->act[nl - 2].hi;
+    h.hl = c->act[nl - 2].lo;
+    h.c0 = c->hc0; h.mT = c->hmT;
+    h.dh = c->dhs[nl - 2].hi; h.dhl = c->dhs[nl - 2].lo;
+    h.dhT = c->dhTs[nl - 2].hi; h.dhTl = c->dhTs[nl - 2].lo; h.ldt = Bp;
+    h.acc = c->hacc; h.accU = c->haccU;
+    h.gW = c->grad + c->woff[nl - 1];
+    h.gb = h.gW + (int64_t)w * H;
+    prof_begin(c);
+    head_means_kernel<<<h.T + 1, w, 0, c->stream>>>(h);
+    if ((s = launch_check(c, HRP_K_HEAD_BWD))) return s;
+    if (conc && (s = fork(c))) return s;
+    auto wgrad = [&]() -> hrp_status {
+      CK(cudaMemsetAsync(c->hacc, 0, sizeof(double) * (size_t)H * (w + 1), c->stream));
+      CK(cudaMemsetAsync(c->haccU, 0, sizeof(double) * (size_t)h.T * (w + 1), c->stream));
+      const int chunks = (w + 1 + kHeadCols - 1) / kHeadCols;
+      const int spc = std::max(16, std::min(256, B * chunks / (4 * 148) + 1));
+      prof_begin(c);
+      head_scatter_kernel<<<dim3(chunks, (B + spc - 1) / spc), kHeadCols,
+                            (size_t)h.T * kHeadCols * sizeof(double), c->stream>>>(h, spc);
+      hrp_status t = launch_check(c, HRP_K_HEAD_BWD);
+      if (t) return t;
+      const int64_t n = (int64_t)H * (w + 1);
+      prof_begin(c);
+      head_finalize_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(h);
+      return launch_check(c, HRP_K_HEAD_BWD);
+    };
+    s = conc ? on_side(c, wgrad) : wgrad();
+    if (s) return s;
+    prof_begin(c);
+    head_dgrad_kernel<<<dim3((w + kHeadCols - 1) / kHeadCols, (B + kHeadRows - 1) / kHeadRows), 256,
+                        0, c->stream>>>(h);
+    if ((s = launch_check(c, HRP_K_HEAD_BWD))) return s;
+    if (conc && (s = fork(c))) return s;
+    dY = c->dhs[nl - 2];
+    dYT = c->dhTs[nl - 2];
+    ldy = w;
+    top = nl - 2;
+  } else {
+    if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, c->ldz, c->dz, c->dzT, Bp))) return s;
+    if (conc && (s = fork(c))) return s;
+  }
+  for (int i = top; i >= 0; --i) {    const int fi = c->dims[i], fo = c->dims[i + 1];
     const Pl HinT = (i == 0) ? c->XT : c->actT[i - 1];
     float* gW = c->grad + c->woff[i];
     float* gb = gW + (int64_t)fi * fo;
@@ -806,6 +861,19 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
         CK(cudaMemsetAsync(q, 0, sizeof(float) * Bp * wd, c->stream));
     }
   }
+  if (split) {
+    c->head_struct = true;
+    const int T = hs.T;
+    CK(ar.alloc((void**)&c->hdesc, sizeof(int) * 8 * (size_t)B));
+    CK(ar.alloc((void**)&c->hacc, sizeof(double) * (size_t)H * (wd + 1)));
+    CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)T * (wd + 1)));
+    CK(ar.alloc((void**)&c->hc0, sizeof(float) * wd));
+    CK(ar.alloc((void**)&c->hmT, sizeof(float) * (size_t)T * wd));
+    if ((size_t)T * kHeadCols * sizeof(double) > 200 * 1024)
+      return fail(HRP_ERANGE, "structured head backward: too many slot types");
+    CK(cudaFuncSetAttribute(head_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)((size_t)T * kHeadCols * sizeof(double))));
+  }
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
@@ -1005,8 +1073,9 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.gamma = c->cfg.gamma;
   t.inv_btot = 1.f / ((float)B * (float)c->world);
   t.explicit_mode = c->explicit_mode;
-  t.dz = c->dz.hi;
-  t.dz_lo = c->dz.lo;
+  t.dz = c->head_struct ? nullptr : c->dz.hi;
+  t.dz_lo = c->head_struct ? nullptr : c->dz.lo;
+  t.hdesc = c->hdesc;
   t.ldz = c->ldz;
   t.dsq = c->dsq;
   t.astar = d_astar;

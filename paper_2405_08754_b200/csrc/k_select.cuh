@@ -826,6 +826,23 @@ __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) t
       if (a.astar) a.astar[b] = astar;
     }
     const float sc = delta * a.inv_btot;
+    if (a.dz == nullptr) {
+      // structured head gradient: dQ/dz has 1 + 1 + C non-constant entries per sample (v,
+      // aL[l], aJ[g_i][t_i]) plus the two duelling-mean terms; the head backward kernels
+      // (k_head.cuh) expand it without materialising dz
+      if (lane < 8) {
+        int v = 0;
+        if (lane == 0) v = __float_as_int(sc);
+        else if (lane == 1) v = 1 + l;
+        else if (lane == 2) v = C;
+        else if (lane < 7) v = lane - 3 < C ? 1 + L + g[lane - 3] * T + tt[lane - 3] : -1;
+        else v = (tt[0] & 255) | (C > 1 ? (tt[1] & 255) << 8 : 0) |
+                 (C > 2 ? (tt[2] & 255) << 16 : 0) | (C > 3 ? (tt[3] & 255) << 24 : 0);
+        a.hdesc[(size_t)b * 8 + lane] = v;
+      }
+      __syncwarp();
+      continue;
+    }
     const float invL = 1.f / (float)L, invW = 1.f / (float)W;
     float* dzr = a.dz + (size_t)b * a.ldz;
     float* dzl = a.dz_lo ? a.dz_lo + (size_t)b * a.ldz : nullptr;

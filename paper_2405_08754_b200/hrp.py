@@ -240,7 +240,7 @@ def hrp_set_weights(ctx, w):
 
 
 KERNEL_CLASSES = ["encode", "gemm_fwd", "gemm_bwd", "select", "td", "sample", "sgd", "misc",
-                  "allreduce"]
+                  "allreduce", "head_bwd"]
 
 
 def hrp_profile(ctx, enable):

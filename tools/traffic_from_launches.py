@@ -22,7 +22,7 @@ def klass(name):
                      ("sample_kernel", "sample"), ("sgd", "sgd"), ("split_kernel", "sgd"),
                      ("split_t_kernel", "sgd"), ("reduce_splits", "gemm_bwd"),
                      ("rowsum", "gemm_bwd"), ("transpose_kernel", "gemm_bwd"),
-                     ("loss_kernel", "misc"), ("brute_kernel", "brute")):
+                     ("loss_kernel", "misc"), ("brute_kernel", "brute"), ("head_", "head_bwd")):
         if key in name:
             return cls
     return None
