@@ -285,7 +285,8 @@ struct hrp_ctx {
   bool head_struct = false;
   int* hdesc = nullptr;               // [B][8]
   double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
-  float *hc0 = nullptr, *hmT = nullptr;      // [w], [T][w]
+  float *hc0 = nullptr, *hmT = nullptr;      // online head duelling-mean rows [w + 1], [T][w + 1]
+  float *hc0t = nullptr, *hmTt = nullptr;    // target head
   uint8_t* bwin = nullptr;            // [2B][W] or [chunk][W]
   uint64_t* bsched = nullptr;
   int64_t* bact = nullptr;
@@ -456,8 +457,11 @@ bool tc_mode(const hrp_ctx* c) { return c->gemm_mode == 2 && c->tc; }
 // pass), head output z_out [M][H] (raw).  With t_rows > 0 the first t_rows rows of every hidden
 // output are also stored transposed in c->actT (operands of the weight-gradient GEMMs).
 // Tensor-core path: X and the hidden outputs are hi/lo planes; SIMT path: raw (hi only).
+// head_from: the head layer runs on rows [head_from, M) only (its output rows keep their
+// offsets in z_out); head_from >= M skips it (the structured update needs the head only where
+// every action is scored).
 hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out,
-                       int t_rows = 0, const std::vector<Pl>* acts = nullptr) {
+                       int t_rows = 0, const std::vector<Pl>* acts = nullptr, int head_from = 0) {
   const std::vector<Pl>& act = acts ? *acts : c->act;
   c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
@@ -470,6 +474,13 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out
     const float* b = Wm + (int64_t)fi * fo;
     const Pl out = (i == nl - 1) ? Pl{z_out, nullptr} : act[i];
     hrp_status s;
+    if (i == nl - 1 && head_from > 0) {
+      if (head_from >= M) return HRP_OK;
+      const Pl hs = h.off((size_t)head_from * ldh);
+      const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
+      return tc_run(c, HRP_K_GEMM_FWD, TC_EPI_BIAS, M - head_from, fo, fi, hs.c(), ldh, hi,
+                    hi + c->sstride, b, nullptr, 0, Pl{z_out + (size_t)head_from * fo, nullptr});
+    }
     if (tc_mode(c)) {
       const Pl outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : Pl{};
       const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
@@ -507,6 +518,7 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
     h.B = B; h.w = w; h.H = H; h.L = c->hs.L; h.T = c->hs.T; h.W = c->hs.W;
     h.hdesc = c->hdesc;
     h.Wh = c->theta + c->woff[nl - 1];
+    h.bh = h.Wh + (int64_t)w * H;
     h.hh = c->act[nl - 2].hi;
     h.hl = c->act[nl - 2].lo;
     h.c0 = c->hc0; h.mT = c->hmT;
@@ -515,20 +527,17 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
     h.acc = c->hacc; h.accU = c->haccU;
     h.gW = c->grad + c->woff[nl - 1];
     h.gb = h.gW + (int64_t)w * H;
-    prof_begin(c);
-    head_means_kernel<<<h.T + 1, w, 0, c->stream>>>(h);
-    if ((s = launch_check(c, HRP_K_HEAD_BWD))) return s;
     if (conc && (s = fork(c))) return s;
     auto wgrad = [&]() -> hrp_status {
       CK(cudaMemsetAsync(c->hacc, 0, sizeof(double) * (size_t)H * (w + 1), c->stream));
-      CK(cudaMemsetAsync(c->haccU, 0, sizeof(double) * (size_t)h.T * (w + 1), c->stream));
-      const int chunks = (w + 1 + kHeadCols - 1) / kHeadCols;
-      const int spc = std::max(16, std::min(256, B * chunks / (4 * 148) + 1));
+      const int spc = std::max(4, std::min(64, B / (4 * 148) + 1));
       prof_begin(c);
-      head_scatter_kernel<<<dim3(chunks, (B + spc - 1) / spc), kHeadCols,
-                            (size_t)h.T * kHeadCols * sizeof(double), c->stream>>>(h, spc);
+      head_scatter_kernel<<<(B + spc - 1) / spc, 256, 0, c->stream>>>(h, spc);
       hrp_status t = launch_check(c, HRP_K_HEAD_BWD);
       if (t) return t;
+      prof_begin(c);
+      head_su_kernel<<<dim3(h.T + 1, (w + 1 + 31) / 32), 256, 0, c->stream>>>(h);
+      if ((t = launch_check(c, HRP_K_HEAD_BWD))) return t;
       const int64_t n = (int64_t)H * (w + 1);
       prof_begin(c);
       head_finalize_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(h);
@@ -866,13 +875,11 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     const int T = hs.T;
     CK(ar.alloc((void**)&c->hdesc, sizeof(int) * 8 * (size_t)B));
     CK(ar.alloc((void**)&c->hacc, sizeof(double) * (size_t)H * (wd + 1)));
-    CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)T * (wd + 1)));
-    CK(ar.alloc((void**)&c->hc0, sizeof(float) * wd));
-    CK(ar.alloc((void**)&c->hmT, sizeof(float) * (size_t)T * wd));
-    if ((size_t)T * kHeadCols * sizeof(double) > 200 * 1024)
-      return fail(HRP_ERANGE, "structured head backward: too many slot types");
-    CK(cudaFuncSetAttribute(head_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)((size_t)T * kHeadCols * sizeof(double))));
+    CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)(T + 1) * (wd + 1)));
+    CK(ar.alloc((void**)&c->hc0, sizeof(float) * (wd + 1)));
+    CK(ar.alloc((void**)&c->hmT, sizeof(float) * (size_t)T * (wd + 1)));
+    CK(ar.alloc((void**)&c->hc0t, sizeof(float) * (wd + 1)));
+    CK(ar.alloc((void**)&c->hmTt, sizeof(float) * (size_t)T * (wd + 1)));
   }
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -1050,13 +1057,31 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   // target net on s' beside it (its own activation scratch)
   const bool conc = concurrent(c);
   if (conc && (s = fork(c))) return s;
-  auto target_pass = [&]() {
-    return mlp_forward(c, c->theta_t, c->X.off((size_t)B * c->ldX), B, c->zt, 0, &c->act_t);
+  // structured head: the target net needs only its hidden layers on s' (td evaluates
+  // Q_target(s', a*) from the last hidden row), the online net its head only on the s' rows
+  // (argmax over every action); the duelling-mean rows of both heads go beside them
+  const int nl = (int)c->dims.size() - 1;
+  const int hw = c->dims[nl - 1];
+  auto head_means = [&](const float* th, float* c0, float* mT) {
+    const float* Wh = th + c->woff[nl - 1];
+    prof_begin(c);
+    head_means_kernel<<<dim3(c->hs.T + 1, (hw + 1 + 31) / 32), 256, 0, c->stream>>>(
+        Wh, Wh + (int64_t)hw * H, hw, c->hs.L, c->hs.T, c->hs.W, c0, mT);
+    return launch_check(c, HRP_K_HEAD_BWD);
+  };
+  auto target_pass = [&]() -> hrp_status {
+    hrp_status t = mlp_forward(c, c->theta_t, c->X.off((size_t)B * c->ldX), B, c->zt, 0, &c->act_t,
+                               c->head_struct ? B : 0);
+    if (t || !c->head_struct) return t;
+    if ((t = head_means(c->theta_t, c->hc0t, c->hmTt))) return t;
+    return head_means(c->theta, c->hc0, c->hmT);
   };
   if (conc) {
     if ((s = on_side(c, target_pass))) return s;
   }
-  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, tcb ? B : 0))) return s;
+  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, tcb ? B : 0, nullptr,
+                       c->head_struct ? B : 0)))
+    return s;
   if (conc) {
     if ((s = join(c))) return s;
   } else if ((s = target_pass())) {
@@ -1076,6 +1101,18 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.dz = c->head_struct ? nullptr : c->dz.hi;
   t.dz_lo = c->head_struct ? nullptr : c->dz.lo;
   t.hdesc = c->hdesc;
+  if (c->head_struct) {
+    t.hs_hi = c->act[nl - 2].hi;
+    t.hs_lo = c->act[nl - 2].lo;
+    t.ht_hi = c->act_t[nl - 2].hi;
+    t.ht_lo = c->act_t[nl - 2].lo;
+    t.Wo = c->theta + c->woff[nl - 1];
+    t.bo = t.Wo + (int64_t)hw * H;
+    t.Wt = c->theta_t + c->woff[nl - 1];
+    t.bt = t.Wt + (int64_t)hw * H;
+    t.c0o = c->hc0; t.mTo = c->hmT; t.c0t = c->hc0t; t.mTt = c->hmTt;
+    t.w = hw;
+  }
   t.ldz = c->ldz;
   t.dsq = c->dsq;
   t.astar = d_astar;

@@ -226,6 +226,22 @@ struct TdArgs {
                         //   {sc bits, 1 + l, C, rows 1 + L + g_i T + t_i (i < C; -1 pad) x 4,
                         //    t_0 | t_1 << 8 | t_2 << 16 | t_3 << 24}, sc = delta / (B world)
   int64_t* astar;       // [B] optional
+  // sparse Q (hdesc mode): Q(s, a) and Q_target(s', a*) from the last hidden activations and the
+  // head rows they need, Q = h . (c0 + W[1 + l] + sum_i (W[r_i] - mT[t_i])) + (same on biases),
+  // instead of full online-head rows for s and target-head rows for s'
+  const float* hs_hi;   // online last hidden activation of the s rows [B][w], hi / lo planes
+  const float* hs_lo;
+  const float* ht_hi;   // target last hidden activation of the s' rows [B][w]
+  const float* ht_lo;
+  const float* Wo;      // online head [H][w], biases [H]
+  const float* bo;
+  const float* Wt;      // target head
+  const float* bt;
+  const float* c0o;     // [w + 1], [T][w + 1] duelling-mean rows (head_means_kernel)
+  const float* mTo;
+  const float* c0t;
+  const float* mTt;
+  int w;
   unsigned long long* n_evals;
   unsigned* ctr;        // dynamic row scheduler (self-resetting, zero at create)
 };

@@ -791,6 +791,48 @@ __device__ inline float pwarp_qfloat(const DevSpace& sp, const PTabs& tb, PWarpS
   return q;
 }
 
+// Action idx -> layout, members g_i and their slot types t_i (returns l; C = nsl[l]).
+__device__ __forceinline__ int decode_types(const DevSpace& sp, const PTabs& tb, int64_t idx,
+                                            int* g, int* t) {
+  int sg[4];
+  const int l = decode_action(sp, idx, g, sg);
+  const uint32_t ty = tb.stype[l];
+  for (int i = 0; i < tb.nsl[l]; ++i) t[i] = (ty >> (8 * sg[i])) & 255;
+  return l;
+}
+
+// Q of action (l, g, t) from a last-hidden row h (hi + lo planes) and the head rows it needs:
+// h . (c0 + W[1 + l] + sum_i (W[r_i] - mT[t_i])) + (c0 + b[1 + l] + sum_i (b[r_i] - mT[t_i]))[w],
+// r_i = 1 + L + g_i T + t_i -- the duelling Q of R1 without the other H - 2 - C head outputs.
+// One warp; result in all lanes.
+__device__ inline float pwarp_qsparse(const DevSpace& sp, int l, int C, const int* g, const int* t,
+                                      const float* __restrict__ hh, const float* __restrict__ hl,
+                                      const float* __restrict__ Wh, const float* __restrict__ bh,
+                                      const float* __restrict__ c0, const float* __restrict__ mT,
+                                      int w) {
+  const int lane = threadIdx.x & 31;
+  const int w1 = w + 1;
+  int r[4] = {0, 0, 0, 0}, tt[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < C) { r[i] = 1 + sp.L + g[i] * sp.T + t[i]; tt[i] = t[i]; }
+  float acc = 0.f;
+  for (int k = lane; k < w; k += 32) {
+    float c = c0[k] + Wh[(size_t)(1 + l) * w + k];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < C) c += Wh[(size_t)r[i] * w + k] - mT[(size_t)tt[i] * w1 + k];
+    acc += (hh[k] + hl[k]) * c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  float bsum = c0[w] + bh[1 + l];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < C) bsum += bh[r[i]] - mT[(size_t)tt[i] * w1 + w];
+  return acc + bsum;
+}
+
 template <int X>
 __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) td_kernel(DevSpace sp, TdArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -810,15 +852,28 @@ __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) t
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
-      const float* tg = a.z_tgt + (size_t)b * H;
-      const float qt = pwarp_qfloat(sp, tb, w, tg, astar,
-                                    nullptr, nullptr, nullptr);
+      float qt;
+      if (a.dz == nullptr) {
+        int gs[4], ts[4];
+        const int ls = decode_types(sp, tb, astar, gs, ts);
+        qt = pwarp_qsparse(sp, ls, tb.nsl[ls], gs, ts, a.ht_hi + (size_t)b * a.w,
+                           a.ht_lo + (size_t)b * a.w, a.Wt, a.bt, a.c0t, a.mTt, a.w);
+      } else {
+        const float* tg = a.z_tgt + (size_t)b * H;
+        qt = pwarp_qfloat(sp, tb, w, tg, astar, nullptr, nullptr, nullptr);
+      }
       y = a.br[b] + a.gamma * qt;
     }
     int l, g[4], tt[4];
-    const float* og = a.z_all + (size_t)b * H;
-    const float q = pwarp_qfloat(sp, tb, w, og, a.bact[b], &l,
-                                 g, tt);
+    float q;
+    if (a.dz == nullptr) {
+      l = decode_types(sp, tb, a.bact[b], g, tt);
+      q = pwarp_qsparse(sp, l, tb.nsl[l], g, tt, a.hs_hi + (size_t)b * a.w,
+                        a.hs_lo + (size_t)b * a.w, a.Wo, a.bo, a.c0o, a.mTo, a.w);
+    } else {
+      const float* og = a.z_all + (size_t)b * H;
+      q = pwarp_qfloat(sp, tb, w, og, a.bact[b], &l, g, tt);
+    }
     const int C = tb.nsl[l];
     const float delta = q - y;
     if (lane == 0) {
