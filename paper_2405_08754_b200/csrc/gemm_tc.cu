@@ -576,7 +576,9 @@ hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes
                          float* ws, size_t ws_elems, float* D, float* db) {
   // D[M][N] = A[M][K] . B[N][K]^T, split-K + deterministic reduce
   const long tiles = (long)((M + BM - 1) / BM) * ((N + 127) / 128);
-  int S = (int)std::max(1L, std::min(32L, (2L * g->nsm + tiles - 1) / tiles));
+  // one wave: tiles x S <= SMs (each CTA holds one SM; a second partial wave costs a whole CTA
+  // time for a few tiles, and every extra split adds an M x N partial to the reduction)
+  int S = (int)std::max(1L, std::min(64L, (long)g->nsm / tiles));
   int kc = (K + S - 1) / S;
   kc = (kc + BK - 1) / BK * BK;
   S = (K + kc - 1) / kc;

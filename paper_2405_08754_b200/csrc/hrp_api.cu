@@ -809,8 +809,14 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->theta_t, sizeof(float) * o));
   CK(ar.alloc((void**)&c->grad, sizeof(float) * o));
   size_t ws = 0;
-  for (size_t i = 0; i + 1 < c->dims.size(); ++i)
-    ws = std::max(ws, (size_t)32 * (c->dims[i] + 1) * c->dims[i + 1]);
+  for (size_t i = 0; i + 1 < c->dims.size(); ++i) {
+    // split-K partials of the weight-gradient GEMM [fo][fi + 1] (tc_gemm_wgrad: one wave,
+    // at most 64 splits, 128 x 128 tiles)
+    const size_t fo = c->dims[i + 1], fi1 = c->dims[i] + 1;
+    const size_t tiles = ((fo + 127) / 128) * ((fi1 + 127) / 128);
+    const size_t S = std::max<size_t>(1, std::min<size_t>(64, (size_t)nsm / tiles));
+    ws = std::max(ws, S * fo * fi1);
+  }
   c->ws_splitk_elems = ws;
   CK(ar.alloc((void**)&c->ws_splitk, sizeof(float) * ws));
   CK(ar.alloc((void**)&c->win, (size_t)E * W));
