@@ -284,6 +284,7 @@ struct hrp_ctx {
   // instead of the dense dz, the head's two backward GEMMs become gathers / scatters
   bool head_struct = false;
   int* hdesc = nullptr;               // [B][8]
+  int* tdesc = nullptr;               // [B][8] (a* on s')
   double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
   float *hc0 = nullptr, *hmT = nullptr;      // online head duelling-mean rows [w + 1], [T][w + 1]
   float *hc0t = nullptr, *hmTt = nullptr;    // target head
@@ -880,6 +881,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     c->head_struct = true;
     const int T = hs.T;
     CK(ar.alloc((void**)&c->hdesc, sizeof(int) * 8 * (size_t)B));
+    CK(ar.alloc((void**)&c->tdesc, sizeof(int) * 8 * (size_t)B));
     CK(ar.alloc((void**)&c->hacc, sizeof(double) * (size_t)H * (wd + 1)));
     CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)(T + 1) * (wd + 1)));
     CK(ar.alloc((void**)&c->hc0, sizeof(float) * (wd + 1)));
@@ -1107,6 +1109,7 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.dz = c->head_struct ? nullptr : c->dz.hi;
   t.dz_lo = c->head_struct ? nullptr : c->dz.lo;
   t.hdesc = c->hdesc;
+  t.tdesc = c->tdesc;
   if (c->head_struct) {
     t.hs_hi = c->act[nl - 2].hi;
     t.hs_lo = c->act[nl - 2].lo;
@@ -1133,6 +1136,11 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
 #undef HRP_TD
   }
   if ((s = launch_check(c, HRP_K_TD))) return s;
+  if (c->head_struct) {
+    prof_begin(c);
+    tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(t);
+    if ((s = launch_check(c, HRP_K_TD))) return s;
+  }
   prof_begin(c);
   loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
   if ((s = launch_check(c, HRP_K_MISC))) return s;

@@ -15,8 +15,10 @@
 //           into registers once and walks the C! permutations unrolled at compile time, so a
 //           (set, l, sigma) evaluation is C register maxes for the compute term plus C memw
 //           lookups -- no atomics.  Feasible iff CoRun <= Solo(B); the lowest (CoRun, action
-//           index) is kept per lane (ascending index order, strict <), then warp-reduced as a
-//           packed key (CoRun << 26 | idx) and stored once.
+//           index) is kept per lane, then warp-reduced as a packed key (CoRun << 26 | idx) and
+//           stored once.  Layouts are ordered by their number of memory domains nd inside a
+//           group: the memory term needs nd lookups per permutation (one per layout when
+//           nd = 1), and a warp's lanes mostly share nd.
 //  phase 2  subset DP over the 2^W sets, level by level in popcount order:
 //           OPT(S) = min over B containing min(S) of best(B) + OPT(S \ B), ties broken by the
 //           block-order rule (prefer the block whose W-bit reversal is larger, reading R21b).
@@ -57,6 +59,33 @@ __host__ __device__ inline size_t brute_smem_bytes(int W, int T, int n_items) {
   return S * 8 /*bestkey*/ + S * 8 /*dp*/ + (size_t)n_items * 4 + 512 * 8 /*layout tables*/ +
          (size_t)(kBruteThreads / 32) * 64 * 4 /*memw*/ + (size_t)W * T * 4 /*tc*/ +
          S * 2 /*choice*/ + 64;
+}
+
+// The C! permutations of one (set, layout), unrolled: compute term from the register matrix Mc,
+// memory term from the ND distinct memory domains of the layout (ND = 1: one lookup hoisted
+// out of the walk).  Keeps the lowest (CoRun, index).
+template <int C, int ND>
+__device__ __forceinline__ void perm_walk(const uint32_t (&Mc)[C][C], const uint32_t* mrow,
+                                          const uint32_t* memw, uint32_t ofi, uint32_t& bcr,
+                                          uint32_t& bidx) {
+  constexpr int F = fact_c(C);
+  uint32_t mem1 = 0;
+  if (ND == 1) mem1 = memw_at(memw, mrow[0], 0);
+#pragma unroll
+  for (int pp = 0; pp < F; ++pp) {
+    uint32_t cr = Mc[0][perm_elem_c(C, pp, 0)];
+#pragma unroll
+    for (int i = 1; i < C; ++i) cr = max(cr, Mc[i][perm_elem_c(C, pp, i)]);
+    if (ND == 1) {
+      cr = max(cr, mem1);
+    } else {
+      const uint32_t mi = mrow[pp];
+#pragma unroll
+      for (int d = 0; d < ND; ++d) cr = max(cr, memw_at(memw, mi, d));
+    }
+    const uint32_t idx = ofi + pp;
+    if (cr < bcr || (cr == bcr && idx < bidx)) { bcr = cr; bidx = idx; }
+  }
 }
 
 // One job set (members packed in memb, lex rank r among the C-sets) by one warp; lane <-> layout.
@@ -100,9 +129,9 @@ __device__ __forceinline__ void brute_set(int lane, uint32_t memb, int r, int nl
     memw[e] = v;
   }
   __syncwarp();
-  // running best per lane: CoRun < bcr (strict, ascending index order keeps the lowest index);
-  // bcr starts at Solo + 1, so the first accepted evaluation is a feasible one
-  uint32_t bcr = solo + 1, bidx = 0;
+  // running best per lane, (CoRun, index) lexicographic; bcr starts at Solo + 1 (the final
+  // bcr <= Solo test drops lanes that saw no feasible evaluation)
+  uint32_t bcr = solo + 1, bidx = 0xffffffffu;
   for (int li = lane; li < nl; li += 32) {
     const uint32_t ty = lty[li], of = loff[li];
     const uint32_t* mrow = lmi + li * F;
@@ -113,16 +142,12 @@ __device__ __forceinline__ void brute_set(int lane, uint32_t memb, int r, int nl
 #pragma unroll
       for (int i = 0; i < C; ++i) Mc[i][s] = tcw[gT[i] + tau];
     }
-#pragma unroll
-    for (int pp = 0; pp < F; ++pp) {
-      const uint32_t mi = mrow[pp];
-      uint32_t cr = Mc[0][perm_elem_c(C, pp, 0)];
-#pragma unroll
-      for (int i = 1; i < C; ++i) cr = max(cr, Mc[i][perm_elem_c(C, pp, i)]);
-#pragma unroll
-      for (int i = 0; i < C; ++i) cr = max(cr, memw_at(memw, mi, i));
-      if (cr < bcr) { bcr = cr; bidx = of + pp; }
-    }
+    const int nd = of >> 28;                  // layouts are sorted by nd inside the C group
+    const uint32_t ofi = of & 0x0fffffffu;
+    if (nd == 1) perm_walk<C, 1>(Mc, mrow, memw, ofi, bcr, bidx);
+    else if (nd == 2 || C < 3) perm_walk<C, (C < 2 ? 1 : 2)>(Mc, mrow, memw, ofi, bcr, bidx);
+    else if (nd == 3 || C < 4) perm_walk<C, (C < 3 ? 1 : 3)>(Mc, mrow, memw, ofi, bcr, bidx);
+    else perm_walk<C, C>(Mc, mrow, memw, ofi, bcr, bidx);
   }
   unsigned long long best = bcr <= solo
       ? ((unsigned long long)bcr << kBruteIdxBits) | (unsigned long long)(bidx + (uint32_t)r * F)
@@ -156,13 +181,30 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
   __shared__ uint16_t lay_of_c[512];
 
   // ---- setup: the (layout, permutation) item table ----
+  __shared__ uint8_t lns[512], lnd[512];   // per layout: slot count, distinct memory domains
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    const int C = sp.lay_n[l];
+    int n = 0;
+    for (int s2 = 0; s2 < C; ++s2) {
+      bool first = true;
+      for (int s3 = 0; s3 < s2; ++s3)
+        first &= (sp.lay_slot[l * 4 + s3] >> 24) != (sp.lay_slot[l * 4 + s2] >> 24);
+      n += first;
+    }
+    lns[l] = (uint8_t)C;
+    lnd[l] = (uint8_t)n;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    // layouts grouped by slot count C and, inside a group, by their number of distinct memory
+    // domains nd (so a warp's lanes mostly walk permutations of the same shape)
     int k = 0, it = 0;
     for (int C = 1; C <= 4; ++C) {
       ilay[C] = k;
       ibase[C] = it;
-      for (int l = 0; l < L; ++l)
-        if (sp.lay_n[l] == C) { lay_of_c[k++] = (uint16_t)l; it += fact_c(C); }
+      for (int nd = 1; nd <= 4; ++nd)
+        for (int l = 0; l < L; ++l)
+          if (lns[l] == C && lnd[l] == nd) { lay_of_c[k++] = (uint16_t)l; it += fact_c(C); }
     }
     ilay[5] = k;
     ibase[5] = it;
@@ -171,7 +213,7 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
   for (int k = threadIdx.x; k < ilay[5]; k += blockDim.x) {
     const int l = lay_of_c[k];
     lty[k] = sp.lay_stype[l];
-    loff[k] = (uint32_t)sp.off[l];
+    loff[k] = (uint32_t)sp.off[l] | ((uint32_t)lnd[l] << 28);   // off < 2^26 (host-checked)
   }
   for (int C = 1; C <= 4; ++C) {
     const int F = fact_c(C), n = ibase[C + 1] - ibase[C];
@@ -187,11 +229,18 @@ __global__ void __launch_bounds__(kBruteThreads, 1) brute_kernel(DevSpace sp, De
           if ((int)((v >> 16) & 255) == a.b8v[q]) bi[s] = q;
       }
       for (int i = 0; i < C; ++i) sl[i] = perm_elem_c(C, pp, i);
+      // byte d: memw offset of the layout's d-th distinct memory domain (slot order) = (its
+      // memory-size index, the members placed in it by sigma)
       uint32_t mi = 0;
-      for (int i = 0; i < C; ++i) {
+      int d = 0;
+      for (int s2 = 0; s2 < C; ++s2) {
+        bool first = true;
+        for (int s3 = 0; s3 < s2; ++s3) first &= dom[s3] != dom[s2];
+        if (!first) continue;
         uint32_t mm = 0;
-        for (int i2 = 0; i2 < C; ++i2) mm |= (dom[sl[i2]] == dom[sl[i]]) ? 1u << i2 : 0u;
-        mi |= ((uint32_t)(bi[sl[i]] * 16 + mm) * 4) << (8 * i);   // byte offset into memw
+        for (int i = 0; i < C; ++i) mm |= dom[sl[i]] == dom[s2] ? 1u << i : 0u;
+        mi |= ((uint32_t)(bi[s2] * 16 + mm) * 4) << (8 * d);   // byte offset into memw
+        ++d;
       }
       lmi[ibase[C] + t] = mi;
     }

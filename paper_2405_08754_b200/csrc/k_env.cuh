@@ -222,6 +222,7 @@ struct TdArgs {
   float* dz_lo;         // [B][H] lo plane (tensor-core path) or NULL
   int ldz;              // row stride of dz
   float* dsq;           // [B]
+  int* tdesc;           // structured mode: [B][8] descriptor of a* (word 2 = -1 when done)
   int* hdesc;           // structured head gradient (dz == NULL): [B][8] per sample
                         //   {sc bits, 1 + l, C, rows 1 + L + g_i T + t_i (i < C; -1 pad) x 4,
                         //    t_0 | t_1 << 8 | t_2 << 16 | t_3 << 24}, sc = delta / (B world)

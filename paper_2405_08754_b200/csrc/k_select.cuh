@@ -801,24 +801,43 @@ __device__ __forceinline__ int decode_types(const DevSpace& sp, const PTabs& tb,
   return l;
 }
 
-// Q of action (l, g, t) from a last-hidden row h (hi + lo planes) and the head rows it needs:
-// h . (c0 + W[1 + l] + sum_i (W[r_i] - mT[t_i])) + (c0 + b[1 + l] + sum_i (b[r_i] - mT[t_i]))[w],
-// r_i = 1 + L + g_i T + t_i -- the duelling Q of R1 without the other H - 2 - C head outputs.
-// One warp; result in all lanes.
-__device__ inline float pwarp_qsparse(const DevSpace& sp, int l, int C, const int* g, const int* t,
-                                      const float* __restrict__ hh, const float* __restrict__ hl,
-                                      const float* __restrict__ Wh, const float* __restrict__ bh,
-                                      const float* __restrict__ c0, const float* __restrict__ mT,
-                                      int w) {
+// Action descriptor of idx (lanes 1..7 write words 1..7; word 0 is left to tdq_kernel):
+// {-, 1 + l, C, rows 1 + L + g_i T + t_i (i < C; -1 pad), t_0 | t_1 << 8 | t_2 << 16 | t_3 << 24}
+__device__ inline void write_desc(const DevSpace& sp, const PTabs& tb, int64_t idx, int* d) {
+  const int lane = threadIdx.x & 31;
+  int g[4], t[4];
+  const int l = decode_types(sp, tb, idx, g, t);
+  const int C = tb.nsl[l];
+  if (lane >= 1 && lane < 8) {
+    int v;
+    if (lane == 1) v = 1 + l;
+    else if (lane == 2) v = C;
+    else if (lane < 7) v = lane - 3 < C ? 1 + sp.L + g[lane - 3] * sp.T + t[lane - 3] : -1;
+    else v = (t[0] & 255) | (C > 1 ? (t[1] & 255) << 8 : 0) | (C > 2 ? (t[2] & 255) << 16 : 0) |
+             (C > 3 ? (t[3] & 255) << 24 : 0);
+    d[lane] = v;
+  }
+}
+
+// Q of the action in descriptor d from a last-hidden row (hi + lo planes): the sparse duelling
+// Q of pwarp_qsparse.  One warp; result in all lanes.
+__device__ inline float pwarp_qdesc(const int* __restrict__ d, const float* __restrict__ hh,
+                                    const float* __restrict__ hl, const float* __restrict__ Wh,
+                                    const float* __restrict__ bh, const float* __restrict__ c0,
+                                    const float* __restrict__ mT, int w) {
   const int lane = threadIdx.x & 31;
   const int w1 = w + 1;
-  int r[4] = {0, 0, 0, 0}, tt[4] = {0, 0, 0, 0};
+  const int l1 = d[1], C = d[2];
+  const uint32_t tp = (uint32_t)d[7];
+  int r[4], tt[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i < C) { r[i] = 1 + sp.L + g[i] * sp.T + t[i]; tt[i] = t[i]; }
+  for (int i = 0; i < 4; ++i) {
+    r[i] = i < C ? d[3 + i] : 0;
+    tt[i] = (tp >> (8 * i)) & 255;
+  }
   float acc = 0.f;
   for (int k = lane; k < w; k += 32) {
-    float c = c0[k] + Wh[(size_t)(1 + l) * w + k];
+    float c = c0[k] + Wh[(size_t)l1 * w + k];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (i < C) c += Wh[(size_t)r[i] * w + k] - mT[(size_t)tt[i] * w1 + k];
@@ -826,11 +845,32 @@ __device__ inline float pwarp_qsparse(const DevSpace& sp, int l, int C, const in
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  float bsum = c0[w] + bh[1 + l];
+  float bsum = c0[w] + bh[l1];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (i < C) bsum += bh[r[i]] - mT[(size_t)tt[i] * w1 + w];
   return acc + bsum;
+}
+
+// Structured-mode tail of the TD step (a9-a10): warp per sample, y = r + gamma Q_target(s', a*)
+// (y = r when done), delta = Q(s, a) - y; dsq = delta^2, hdesc word 0 = delta / (B world).
+__global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= a.B) return;
+  const int* td = a.tdesc + (size_t)b * 8;
+  int* hd = a.hdesc + (size_t)b * 8;
+  float y = a.br[b];
+  if (td[2] > 0)
+    y += a.gamma * pwarp_qdesc(td, a.ht_hi + (size_t)b * a.w, a.ht_lo + (size_t)b * a.w, a.Wt,
+                               a.bt, a.c0t, a.mTt, a.w);
+  const float q = pwarp_qdesc(hd, a.hs_hi + (size_t)b * a.w, a.hs_lo + (size_t)b * a.w, a.Wo,
+                              a.bo, a.c0o, a.mTo, a.w);
+  const float delta = q - y;
+  if (lane == 0) {
+    a.dsq[b] = delta * delta;
+    hd[0] = __float_as_int(delta * a.inv_btot);
+  }
 }
 
 template <int X>
@@ -846,34 +886,38 @@ __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) t
     const bool done = a.bdone[b] != 0;
     float y = a.br[b];
     int64_t astar = -1;
+    if (a.dz == nullptr) {
+      // structured mode: the argmax a* on s' here; both Q values, delta and the loss terms in
+      // tdq_kernel from the action descriptors (tdesc: a*, hdesc: a)
+      if (!done) {
+        const float* zn = a.z_all + (size_t)(a.B + b) * H;
+        const float meanL = pwarp_means(sp, zn, w.meanJ);
+        int64_t best;
+        greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
+      }
+      if (lane == 0 && a.astar) a.astar[b] = astar;
+      write_desc(sp, tb, a.bact[b], a.hdesc + (size_t)b * 8);
+      if (done) {
+        if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
+      } else {
+        write_desc(sp, tb, astar, a.tdesc + (size_t)b * 8);
+      }
+      __syncwarp();
+      continue;
+    }
     if (!done) {
       const float* zg = a.z_all + (size_t)(a.B + b) * H;
       const float* zn = zg;
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
-      float qt;
-      if (a.dz == nullptr) {
-        int gs[4], ts[4];
-        const int ls = decode_types(sp, tb, astar, gs, ts);
-        qt = pwarp_qsparse(sp, ls, tb.nsl[ls], gs, ts, a.ht_hi + (size_t)b * a.w,
-                           a.ht_lo + (size_t)b * a.w, a.Wt, a.bt, a.c0t, a.mTt, a.w);
-      } else {
-        const float* tg = a.z_tgt + (size_t)b * H;
-        qt = pwarp_qfloat(sp, tb, w, tg, astar, nullptr, nullptr, nullptr);
-      }
+      const float* tg = a.z_tgt + (size_t)b * H;
+      const float qt = pwarp_qfloat(sp, tb, w, tg, astar, nullptr, nullptr, nullptr);
       y = a.br[b] + a.gamma * qt;
     }
     int l, g[4], tt[4];
-    float q;
-    if (a.dz == nullptr) {
-      l = decode_types(sp, tb, a.bact[b], g, tt);
-      q = pwarp_qsparse(sp, l, tb.nsl[l], g, tt, a.hs_hi + (size_t)b * a.w,
-                        a.hs_lo + (size_t)b * a.w, a.Wo, a.bo, a.c0o, a.mTo, a.w);
-    } else {
-      const float* og = a.z_all + (size_t)b * H;
-      q = pwarp_qfloat(sp, tb, w, og, a.bact[b], &l, g, tt);
-    }
+    const float* og = a.z_all + (size_t)b * H;
+    const float q = pwarp_qfloat(sp, tb, w, og, a.bact[b], &l, g, tt);
     const int C = tb.nsl[l];
     const float delta = q - y;
     if (lane == 0) {
@@ -881,23 +925,6 @@ __global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) t
       if (a.astar) a.astar[b] = astar;
     }
     const float sc = delta * a.inv_btot;
-    if (a.dz == nullptr) {
-      // structured head gradient: dQ/dz has 1 + 1 + C non-constant entries per sample (v,
-      // aL[l], aJ[g_i][t_i]) plus the two duelling-mean terms; the head backward kernels
-      // (k_head.cuh) expand it without materialising dz
-      if (lane < 8) {
-        int v = 0;
-        if (lane == 0) v = __float_as_int(sc);
-        else if (lane == 1) v = 1 + l;
-        else if (lane == 2) v = C;
-        else if (lane < 7) v = lane - 3 < C ? 1 + L + g[lane - 3] * T + tt[lane - 3] : -1;
-        else v = (tt[0] & 255) | (C > 1 ? (tt[1] & 255) << 8 : 0) |
-                 (C > 2 ? (tt[2] & 255) << 16 : 0) | (C > 3 ? (tt[3] & 255) << 24 : 0);
-        a.hdesc[(size_t)b * 8 + lane] = v;
-      }
-      __syncwarp();
-      continue;
-    }
     const float invL = 1.f / (float)L, invW = 1.f / (float)W;
     float* dzr = a.dz + (size_t)b * a.ldz;
     float* dzl = a.dz_lo ? a.dz_lo + (size_t)b * a.ldz : nullptr;
