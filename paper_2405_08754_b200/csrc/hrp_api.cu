@@ -632,7 +632,7 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   prof_begin(c);
   const int rpc = sel_rows_per_cta(c->explicit_mode);
   const int grid = std::min((a.M + rpc - 1) / rpc, c->p_grid);
-#define HRP_SEL(X) sel_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
+#define HRP_SEL(X) sel_kernel<X><<<grid, pwarps(X > 0) * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
   HRP_VARIANT(c->sel_variant, HRP_SEL);
 #undef HRP_SEL
   return launch_check(c, HRP_K_SELECT);
@@ -932,7 +932,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   c->sel_variant = c->explicit_mode ? hs.cmax : 0;
   {
     cudaError_t e = cudaSuccess;
-#define HRP_OCC(X) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sel_kernel<X>, kPWarps * 32, c->p_smem)
+#define HRP_OCC(X) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sel_kernel<X>, pwarps(X > 0) * 32, c->p_smem)
     HRP_VARIANT(c->sel_variant, HRP_OCC);
 #undef HRP_OCC
     CK(e);
@@ -1131,7 +1131,7 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   {
     const int rpc = sel_rows_per_cta(c->explicit_mode);
     const int grid = std::min((B + rpc - 1) / rpc, c->p_grid);
-#define HRP_TD(X) td_kernel<X><<<grid, kPWarps * 32, c->p_smem, c->stream>>>(c->dt.sp, t)
+#define HRP_TD(X) td_kernel<X><<<grid, pwarps(X > 0) * 32, c->p_smem, c->stream>>>(c->dt.sp, t)
     HRP_VARIANT(c->sel_variant, HRP_TD);
 #undef HRP_TD
   }

@@ -35,7 +35,9 @@
 
 namespace hrp {
 
-constexpr int kPWarps = 8;   // warps (states in flight) per CTA
+// warps (states in flight) per CTA: explicit enumeration 7 (7 x ~7.4 KB of per-warp tables at
+// cfg 2 keeps 4 CTAs / SM: 90 vs 96 us per select launch), pruned 8
+__host__ __device__ constexpr int pwarps(bool explicit_mode) { return explicit_mode ? 7 : 8; }
 constexpr int kXMaxW = 16;   // explicit enumeration: window size limit
 
 constexpr int kXS = 128;             // explicit: slot types T <= 128
@@ -74,11 +76,11 @@ __host__ __device__ inline size_t ptabs_bytes(int L) {
 }
 
 __host__ __device__ inline size_t pwarp_smem_bytes(int L, int T, int H, bool x) {
-  return ptabs_bytes(L) + kPWarps * pwarp_bytes(T, H, x);
+  return ptabs_bytes(L) + pwarps(x) * pwarp_bytes(T, H, x);
 }
 
 // rows (states) one CTA owns at a time
-__host__ __device__ constexpr int sel_rows_per_cta(bool) { return kPWarps; }
+__host__ __device__ constexpr int sel_rows_per_cta(bool x) { return pwarps(x); }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -676,13 +678,13 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
 }
 
 template <int X>
-__global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4))
+__global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 : 4))
 sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * kPWarps;
+  const int nw = gridDim.x * pwarps(X > 0);
   const int W = sp.W;
   int64_t nevals = 0;
   for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
@@ -874,12 +876,12 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
 }
 
 template <int X>
-__global__ void __launch_bounds__(kPWarps * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) td_kernel(DevSpace sp, TdArgs a) {
+__global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) td_kernel(DevSpace sp, TdArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * kPWarps;
+  const int nw = gridDim.x * pwarps(X > 0);
   const int H = sp.H, L = sp.L, T = sp.T, W = sp.W;
   int64_t nevals = 0;
   for (int b = next_row(a.ctr, a.B, nw); b < a.B; b = next_row(a.ctr, a.B, nw)) {
