@@ -40,7 +40,8 @@ __global__ void encode_kernel(int M, int W, const uint8_t* __restrict__ win,
     const float ic = fW / (float)sc, im = fW / (float)sm, iT = fW / (float)sT;
     float* x = X + (size_t)row * ldx;
     float* xl = Xlo ? Xlo + (size_t)row * ldx : nullptr;
-    for (int i = lane; i < in; i += 32) {
+#pragma unroll 4
+    for (int i = lane; i < in; i += 32) {   // unrolled: 4 independent load chains in flight
       const int j = i / 17, col = i - j * 17;
       const int p = w[j];
       float v;

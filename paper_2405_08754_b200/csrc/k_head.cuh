@@ -88,9 +88,10 @@ __global__ void __launch_bounds__(256) head_dgrad_kernel(HeadArgs a) {
   const int k = k0 + kk;
   if (k < a.w) {
     const float c0 = a.c0[k];   // weight part (k < w)
-    for (int r = threadIdx.x / kHeadCols; r < kHeadRows; r += blockDim.x / kHeadCols) {
-      const int b = b0 + r;
-      if (b >= a.B) break;
+#pragma unroll 4
+    for (int r = threadIdx.x / kHeadCols; r < kHeadRows; r += 256 / kHeadCols) {   // 4 samples'
+      const int b = b0 + r;                                                        // gathers in flight
+      if (b >= a.B) continue;
       const float sc = __int_as_float(desc[r][0]);
       const int C = desc[r][2];
       const uint32_t tp = (uint32_t)desc[r][7];
