@@ -150,9 +150,17 @@ __device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict_
   const float meanL = warp_sum(a) / (float)sp.L;
   const float* aJ = z + 1 + sp.L;
   for (int t = lane; t < sp.T; t += 32) {
-    float s = 0.f;
-    for (int j = 0; j < sp.W; ++j) s += aJ[j * sp.T + t];
-    meanJ[t] = s / (float)sp.W;
+    // four interleaved partial sums (independent load / add chains), combined in fixed order
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int j = 0;
+    for (; j + 4 <= sp.W; j += 4) {
+      s0 += aJ[(j + 0) * sp.T + t];
+      s1 += aJ[(j + 1) * sp.T + t];
+      s2 += aJ[(j + 2) * sp.T + t];
+      s3 += aJ[(j + 3) * sp.T + t];
+    }
+    for (; j < sp.W; ++j) s0 += aJ[j * sp.T + t];
+    meanJ[t] = ((s0 + s1) + (s2 + s3)) / (float)sp.W;
   }
   __syncwarp();
   return meanL;
