@@ -429,7 +429,14 @@ def rooflines(prof, steps, evals, cfg, osp):
         elif name in ("gemm_fwd", "gemm_bwd"):
             rows = E + 3 * B if name == "gemm_fwd" else B
             if name == "gemm_fwd":
-                flops = rows * F
+                if head_struct:
+                    # select forward on E rows (every layer); update: online hidden layers on
+                    # [s; s'] (2B rows) + online head on s' (B) + target hidden layers on s' (B)
+                    Fh = sum(2 * dims[i] * dims[i + 1] for i in range(len(dims) - 2))
+                    Fo = 2 * dims[-2] * dims[-1]
+                    flops = E * F + 3 * B * Fh + B * Fo
+                else:
+                    flops = rows * F
             else:
                 # weight gradients of every GEMM layer + data gradients of all but the first;
                 # with the structured head (class head_bwd) the head layer has no GEMMs
