@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(256) head_means_kernel(const float* __restrict
   else c0[k] = (float)((double)(k < w ? Wh[k] : bh[0]) - tot / L);
 }
 
-constexpr int kHeadRows = 32, kHeadCols = 128;
+constexpr int kHeadRows = 8, kHeadCols = 128;   // 8 samples x 128 columns per CTA: ~7 CTAs / SM at cfg 2
 
-// grid (ceil(w / 128), ceil(B / 32)), 256 threads: 32 samples x 128 columns per CTA.
+// grid (ceil(w / 128), ceil(B / kHeadRows)), 256 threads: kHeadRows samples x 128 columns per CTA.
 __global__ void __launch_bounds__(256) head_dgrad_kernel(HeadArgs a) {
   __shared__ float th[kHeadRows][kHeadCols + 1], tl[kHeadRows][kHeadCols + 1];
   __shared__ int desc[kHeadRows][8];
