@@ -296,7 +296,7 @@ struct hrp_ctx {
   float* dsq = nullptr;
   int64_t* tmp_i64 = nullptr;         // [rows]
   unsigned long long* n_evals = nullptr;
-  unsigned* sched_ctr = nullptr;      // [2] dynamic row schedulers of the select / TD kernels
+  unsigned* sched_ctr = nullptr;      // [4]: row schedulers of the select / TD kernels, tdq ticket
   size_t p_smem = 0;   // warp-per-state selection / TD kernels
   int sel_variant = 0; // 0 pruned argmax, 1..4 explicit enumeration with Cmax = variant
   int p_grid = 0;
@@ -901,8 +901,8 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->tmp_i64, R * 8));
   CK(ar.alloc((void**)&c->n_evals, 16));  // [0] select / inference kernels, [1] TD kernel
   CK(cudaMemsetAsync(c->n_evals, 0, 16, c->stream));
-  CK(ar.alloc((void**)&c->sched_ctr, 2 * sizeof(unsigned)));
-  CK(cudaMemsetAsync(c->sched_ctr, 0, 2 * sizeof(unsigned), c->stream));
+  CK(ar.alloc((void**)&c->sched_ctr, 4 * sizeof(unsigned)));   // select, TD, tdq ticket
+  CK(cudaMemsetAsync(c->sched_ctr, 0, 4 * sizeof(unsigned), c->stream));
   if (init_weights) {
     CK(cudaMemcpyAsync(c->theta, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->theta_t, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
@@ -1050,7 +1050,8 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   const int H = c->hs.head_width();
   hrp_status s;
   prof_begin(c);
-  sample_kernel<<<(B + 127) / 128, 128, 0, c->stream>>>(
+  // one thread per sample, 32 per block: the per-sample decode is latency-bound, spread it
+  sample_kernel<<<(B + 31) / 32, 32, 0, c->stream>>>(
       c->dt.sp, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r, c->rep_done,
       c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx);
   if ((s = launch_check(c, HRP_K_SAMPLE))) return s;
@@ -1137,13 +1138,16 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   }
   if ((s = launch_check(c, HRP_K_TD))) return s;
   if (c->head_struct) {
+    t.loss = d_loss;
+    t.done_ctr = c->sched_ctr + 2;
     prof_begin(c);
     tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(t);
     if ((s = launch_check(c, HRP_K_TD))) return s;
+  } else {
+    prof_begin(c);
+    loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
+    if ((s = launch_check(c, HRP_K_MISC))) return s;
   }
-  prof_begin(c);
-  loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
-  if ((s = launch_check(c, HRP_K_MISC))) return s;
   if ((s = mlp_backward(c, B))) return s;
   if (c->world > 1) {
     prof_begin(c);
@@ -1155,6 +1159,7 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   if (tc_mode(c)) {
     SgdSplitArgs g{};
     g.nl = (int)c->dims.size() - 1;
+    g.nlT = c->head_struct ? g.nl - 1 : g.nl;
     g.n = c->n_params;
     g.lr = c->cfg.lr;
     g.th = c->theta;

@@ -244,6 +244,8 @@ struct TdArgs {
   const float* c0t;
   const float* mTt;
   int w;
+  float* loss;          // structured mode: tdq_kernel's last block writes the loss here
+  unsigned* done_ctr;   //   block ticket counter (zero between launches)
   unsigned long long* n_evals;
   unsigned* ctr;        // dynamic row scheduler (self-resetting, zero at create)
 };
@@ -265,6 +267,8 @@ __global__ void sgd_kernel(int64_t n, float lr, float* __restrict__ th, const fl
 constexpr int kMaxLayers = 9;
 struct SgdSplitArgs {
   int nl;
+  int nlT;                           // layers [0, nlT) also get the transposed split (the
+                                     // structured head's backward reads the raw head weights)
   int64_t n;                         // parameters
   float lr;
   float* th;
@@ -299,6 +303,7 @@ __global__ void sgd_split_kernel(SgdSplitArgs a) {
       a.thi[o] = h;
       a.tlo[o] = lw;
     }
+    if (l >= a.nlT) continue;
     const int64_t ot = a.soffT[l] + (int64_t)cc * ((fo + 3) & ~3) + r;
     a.hiT[ot] = h;
     a.loT[ot] = lw;

@@ -863,24 +863,44 @@ __device__ inline float pwarp_qdesc(const int* __restrict__ d, const float* __re
 }
 
 // Structured-mode tail of the TD step (a9-a10): warp per sample, y = r + gamma Q_target(s', a*)
-// (y = r when done), delta = Q(s, a) - y; dsq = delta^2, hdesc word 0 = delta / (B world).
+// (y = r when done), delta = Q(s, a) - y; dsq = delta^2, hdesc word 0 = delta / (B world).  The
+// last block to finish (ticket counter, reset by that block) reduces the loss = sum dsq / (2B)
+// exactly as loss_kernel does (256 threads, strided partial sums, block tree): same bits.
 __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
+  __shared__ float red[32];
+  __shared__ bool last;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b >= a.B) return;
-  const int* td = a.tdesc + (size_t)b * 8;
-  int* hd = a.hdesc + (size_t)b * 8;
-  float y = a.br[b];
-  if (td[2] > 0)
-    y += a.gamma * pwarp_qdesc(td, a.ht_hi + (size_t)b * a.w, a.ht_lo + (size_t)b * a.w, a.Wt,
-                               a.bt, a.c0t, a.mTt, a.w);
-  const float q = pwarp_qdesc(hd, a.hs_hi + (size_t)b * a.w, a.hs_lo + (size_t)b * a.w, a.Wo,
-                              a.bo, a.c0o, a.mTo, a.w);
-  const float delta = q - y;
-  if (lane == 0) {
-    a.dsq[b] = delta * delta;
-    hd[0] = __float_as_int(delta * a.inv_btot);
+  if (b < a.B) {
+    const int* td = a.tdesc + (size_t)b * 8;
+    int* hd = a.hdesc + (size_t)b * 8;
+    float y = a.br[b];
+    if (td[2] > 0)
+      y += a.gamma * pwarp_qdesc(td, a.ht_hi + (size_t)b * a.w, a.ht_lo + (size_t)b * a.w, a.Wt,
+                                 a.bt, a.c0t, a.mTt, a.w);
+    const float q = pwarp_qdesc(hd, a.hs_hi + (size_t)b * a.w, a.hs_lo + (size_t)b * a.w, a.Wo,
+                                a.bo, a.c0o, a.mTo, a.w);
+    const float delta = q - y;
+    if (lane == 0) {
+      a.dsq[b] = delta * delta;
+      hd[0] = __float_as_int(delta * a.inv_btot);
+    }
   }
+  if (a.loss == nullptr) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(a.done_ctr, 1u);
+    last = t == gridDim.x - 1;
+    if (last) *a.done_ctr = 0;   // ready for the next launch (graph replays included)
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < a.B; i += blockDim.x) acc += ((volatile const float*)a.dsq)[i];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) *a.loss = acc / (2.f * (float)a.B);
 }
 
 template <int X>
