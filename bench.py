@@ -357,6 +357,11 @@ def run_gpu(args, cfg):
                           "parallelism": f"dp{world} (env sharding + NCCL grad allreduce)"},
                "q_evals_per_s": evals * world / (ms / 1e3),
                "q_evals_per_step": evals / args.steps,
+               "q_evals_def": ("valid (state, joint action) pairs covered by the exact argmax of "
+                               "a5 + a9: explicit mode counts every valid action (leaf rows "
+                               "whose exact fp32 suffix-max bound cannot beat the running "
+                               "maximum are not scored one by one); pruned mode counts the "
+                               "Top-list candidates scored"),
                "gpu_launches": int(n_launch),
                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                        "d2h_bytes_per_step": int(d2h)},
@@ -424,7 +429,9 @@ def rooflines(prof, steps, evals, cfg, osp):
             n = evals[0] if name == "select" else evals[1]
             ach = 2.0 * n / sec / 1e12
             per.update(bound="alu", achieved=ach, peak=alu_peak, unit="Tops/s",
-                       frac=ach / alu_peak, work=f"{n / steps:.4g} Q-evals/step x 2 lane-ops",
+                       frac=ach / alu_peak, work=f"{n / steps:.4g} Q-evals/step (valid actions covered) x 2 lane-ops "
+                            "(one add forming the score, one compare), the naive algorithm's "
+                            "cost",
                        peak_src="148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)")
         elif name in ("gemm_fwd", "gemm_bwd"):
             rows = E + 3 * B if name == "gemm_fwd" else B
