@@ -554,6 +554,7 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   const int lane = threadIdx.x & 31;
   const int W = sp.W, T = sp.T;
   const float* aJ = z + 1 + sp.L;
+  const uint64_t freem = (W == 64 ? ~0ull : ((1ull << W) - 1)) & ~sched;
   for (int t = lane; t < T; t += 32) {
     // top-4 by (value desc, position asc): register-only insertion network.  x < x3 (fp32)
     // implies F(x) <= F(x3) = b3 (F is monotone), so most positions are rejected before the
@@ -562,9 +563,10 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
     float x0 = -INFINITY, x1 = -INFINITY, x2 = -INFINITY, x3 = -INFINITY;
     int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
     const float mj = w.meanJ[t];
-    for (int j = 0; j < W; ++j) {
+    for (uint64_t fm = freem; fm; fm &= fm - 1) {   // free positions, ascending (warp-uniform)
+      const int j = __ffsll((long long)fm) - 1;
       const float x = aJ[j * T + t] - mj;
-      if (x < x3 || ((sched >> j) & 1ull)) continue;
+      if (x < x3) continue;
       const int64_t v = fixed_point(x);
       if (v <= b3) continue;  // ties keep the lower position
       b3 = v; j3 = j; x3 = x;
