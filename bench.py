@@ -127,10 +127,61 @@ def run_reference(args, cfg):
 
 # ------------------------------------------------------------------------------------------
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle-reason sampling DURING the timed region (B200_PROFILING.md clocks
+    line). A timed region here is ~10 ms of GPU work, shorter than nvidia-smi's 100 ms
+    sampling period, so NVML is polled from a thread every ~0.5 ms while the host waits on
+    the stream; one sample is always taken at stop(). Falls back to nvidia-smi if NVML is
+    unavailable."""
+
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, dev):
+        import threading
+        self.rows = []
+        self.src = None
         self.p = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [x.strip() for x in vis.split(",") if x.strip()]
+            if ids and len(ids) > dev:
+                tok = ids[dev]
+                h = (nv.nvmlDeviceGetHandleByIndex(int(tok)) if tok.isdigit()
+                     else nv.nvmlDeviceGetHandleByUUID(tok))
+            else:
+                h = nv.nvmlDeviceGetHandleByIndex(dev)
+            self.nv, self.h = nv, h
+            self.smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.bits = (nv.nvmlClocksEventReasonHwSlowdown,
+                         nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         nv.nvmlClocksEventReasonSwThermalSlowdown,
+                         nv.nvmlClocksEventReasonSwPowerCap)
+            self._sample()
+            self.rows.clear()
+            self._t = threading.Thread(target=self._loop, daemon=True)
+            self._t.start()
+            self.src = "nvml"
+        except Exception:
+            self._smi(dev)
+
+    def _sample(self):
+        nv, h = self.nv, self.h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.rows.append((sm, self.smax, [n for n, b in zip(self.NAMES, self.bits) if r & b]))
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.0005)
+
+    def _smi(self, dev):
         self.path = f"/tmp/hrp_clocks_{os.getpid()}.csv"
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -139,31 +190,34 @@ class Clocks:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            self.src = "nvidia-smi"
         except Exception:
             self.p = None
 
     def stop(self):
-        if self.p is None:
+        if self._t is not None:
+            self._stop.set()
+            self._t.join()
+            try:
+                self._sample()
+            except Exception:
+                pass
+        elif self.p is not None:
+            time.sleep(0.25)
+            self.p.terminate()
+            self.p.wait()
+            for ln in open(self.path):
+                f = [x.strip() for x in ln.split(",")]
+                if len(f) >= 7 and f[0].isdigit():
+                    self.rows.append((int(f[0]), int(f[1]),
+                                      [n for k, n in enumerate(self.NAMES)
+                                       if f[3 + k].lower() == "active"]))
+        if not self.rows:
             return None
-        time.sleep(0.15)
-        self.p.terminate()
-        self.p.wait()
-        rows = []
-        for ln in open(self.path):
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) >= 7 and f[0].isdigit():
-                rows.append(f)
-        if not rows:
-            return None
-        sm = [int(r[0]) for r in rows]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for k, n in enumerate(names):
-                if r[3 + k].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]),
-                "reasons": sorted(reasons), "samples": len(rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({n for r in self.rows for n in r[2]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows), "source": self.src}
 
 
 def run_gpu(args, cfg):
