@@ -259,3 +259,21 @@ def canonical(layout: Layout):
             lst.append((Fraction(c, 8), tuple(sorted(next(ci_iter)))))
         parsed.append((alpha, tuple(sorted(lst))))
     return ("mig", tuple(sorted(parsed)))
+
+
+def select_layouts(slot_table, cmax: int, shares) -> list:
+    """Restricted baselines: the layouts of this oracle's own enumeration whose
+    slots are exactly the given (sm800, b8, dom) tuples, in the table's order.  A table entry
+    that is not a valid hierarchical partition raises (so the baseline tables are pinned to the
+    placement rules of R3/R4 and R23)."""
+    full = enumerate_layouts(cmax, shares, True) + enumerate_layouts(cmax, shares, False)
+    by_slots = {}
+    for l in full:
+        by_slots.setdefault(tuple((s.sm800, s.b8, s.dom) for s in l.slots), l)
+    out = []
+    for entry in slot_table:
+        key = tuple(tuple(x) for x in entry)
+        if key not in by_slots:
+            raise ValueError(f"not a valid hierarchical partition: {entry}")
+        out.append(by_slots[key])
+    return out

@@ -103,8 +103,10 @@ def streams_to_dev(st, dev):
     }
 
 
-def bruteforce(scfg, pool, windows, device=0, stream=None):
-    """hrp_bruteforce_optimum on a uint8 [n][W] numpy array; returns numpy outputs."""
+def bruteforce(scfg, pool, windows, device=0, stream=None, layouts=None):
+    """hrp_bruteforce_optimum on a uint8 [n][W] numpy array; returns numpy outputs.
+    layouts: optional explicit layout table [[(sm800, b8, dom), ...], ...] (restricted
+    baselines, P:246-248)."""
     dev = torch.device("cuda", device)
     st = stream or torch.cuda.current_stream(dev)
     w = torch.from_numpy(np.ascontiguousarray(windows, np.uint8)).to(dev)
@@ -113,7 +115,7 @@ def bruteforce(scfg, pool, windows, device=0, stream=None):
     solo = torch.empty(n, dtype=torch.int64, device=dev)
     rgs = torch.empty((n, W), dtype=torch.uint8, device=dev)
     bact = torch.empty((n, W), dtype=torch.int64, device=dev)
-    hrp.hrp_bruteforce_optimum(space_of(scfg), hrp.make_profiles(pool), n, w, best, solo, rgs,
+    hrp.hrp_bruteforce_optimum(space_of(scfg, layouts), hrp.make_profiles(pool), n, w, best, solo, rgs,
                                bact, st.cuda_stream)
     torch.cuda.synchronize(dev)
     return best.cpu().numpy(), solo.cpu().numpy(), rgs.cpu().numpy(), bact.cpu().numpy()

@@ -18,8 +18,9 @@ All random numbers come from numpy's counter-based Philox generator, seeded with
 from .pool import (TABLE_IV, TABLE_V, UNSEEN, Pool, make_pool, class_counts)
 from .streams import (SEED, philox, make_windows, table_v_windows, step_streams,
                       eps_threshold, init_weights, sched_states)
-from .configs import CONFIGS, SpaceCfg, NetCfg, config
+from .configs import CONFIGS, SpaceCfg, NetCfg, config, MIG_ONLY_LAYOUTS, BASELINE_SPACES
 
 __all__ = ["TABLE_IV", "TABLE_V", "UNSEEN", "Pool", "make_pool", "class_counts", "SEED",
            "philox", "make_windows", "table_v_windows", "step_streams", "eps_threshold",
-           "init_weights", "sched_states", "CONFIGS", "SpaceCfg", "NetCfg", "config"]
+           "init_weights", "sched_states", "CONFIGS", "SpaceCfg", "NetCfg", "config",
+           "MIG_ONLY_LAYOUTS", "BASELINE_SPACES"]

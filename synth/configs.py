@@ -63,5 +63,19 @@ CONFIGS = {
 }
 
 
+# The paper's compared methods as search spaces for the exhaustive optimum at
+# config 3's window (W = 12, Cmax = 4).  "MIG Only (C = 2)" explores the two options
+# of Fig. 2: [{0.375}+{0.5},1m] (one 7-slice GI, CIs of 4 and 3 GPCs sharing its 8
+# memory eighths) and [{0.375},0.5m]+[{0.5},0.5m] (GIs of 4 and 3 GPCs, 4 memory eighths and
+# a memory domain each), plus the whole GPU for a job left alone (= time sharing).
+# Slots are (sm800, b8, domain) in R6's units; this is an input table, not arithmetic.
+MIG_ONLY_LAYOUTS = [[(800, 8, 0)], [(400, 8, 0), (300, 8, 0)], [(400, 4, 0), (300, 4, 1)]]
+BASELINE_SPACES = {
+    "mig_only": (SpaceCfg(12, 2, S10), MIG_ONLY_LAYOUTS),
+    "mps_only": (SpaceCfg(12, 4, S10, mig=False), None),
+    "mig_mps": (SpaceCfg(12, 4, S10), None),
+}
+
+
 def config(k: int) -> Config:
     return CONFIGS[k]

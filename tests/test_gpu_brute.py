@@ -14,10 +14,11 @@ pytestmark = pytest.mark.gpu
 S10 = tuple(range(10, 100, 10))
 
 
-def _cmp(scfg, pool, wins):
+def _cmp(scfg, pool, wins, layouts=None):
     from paper_2405_08754_b200.session import bruteforce
-    best, solo, rgs, bact = bruteforce(scfg, pool, wins)
-    sp = SP.build_space(scfg.window, scfg.cmax, scfg.shares, scfg.mig)
+    best, solo, rgs, bact = bruteforce(scfg, pool, wins, layouts=layouts)
+    L = SP.select_layouts(layouts, scfg.cmax, scfg.shares) if layouts else None
+    sp = SP.build_space(scfg.window, scfg.cmax, scfg.shares, scfg.mig, layouts=L)
     for i, w in enumerate(wins):
         ref = BR.dp_opt(sp, [int(x) for x in w], pool, scfg.interference_q3)
         assert best[i] == ref["cost"], i
@@ -70,3 +71,12 @@ def test_config3_full_launch_sampled():
         ref = BR.dp_opt(sp, [int(x) for x in wins[i]], pool)
         assert (best[i], solo[i], list(rgs[i]), list(bact[i])) == \
             (ref["cost"], ref["solo"], ref["rgs"], ref["block_action"])
+
+
+@pytest.mark.parametrize("name", ["mig_only", "mps_only"])
+def test_restricted_baselines_table_v(name):
+    # P:245-248 compared methods (synth.BASELINE_SPACES) on Q1-Q12: MIG Only through an
+    # explicit layout table (Fig. 2's two options), MPS Only through the MIG-off space
+    pool = synth.make_pool(27)
+    scfg, lay = synth.BASELINE_SPACES[name]
+    _cmp(scfg, pool, synth.table_v_windows(pool), layouts=lay)

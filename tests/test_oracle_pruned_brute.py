@@ -112,3 +112,32 @@ def test_cmax1_is_time_sharing_and_monotone():
     full = BR.dp_opt(SP.build_space(8, 3, S10), win, pool)["cost"]
     mps = BR.dp_opt(SP.build_space(8, 3, S10, mig=False), win, pool)["cost"]
     assert full <= mps
+
+
+def test_restricted_baseline_spaces_table_v():
+    # The compared methods of P:245-248 as search spaces (synth.BASELINE_SPACES): MIG Only
+    # (C = 2, Fig. 2's two options), MPS Only (C <= 4), MIG+MPS (C <= 4).  The MIG-only table
+    # entries must be valid hierarchical partitions of the oracle's own enumeration; each
+    # baseline's optimum is a minimum over a subset of the full space's choices, so it is never
+    # better than MIG+MPS, and never worse than time sharing (ratio >= 1).
+    sc, lay = synth.BASELINE_SPACES["mig_only"]
+    L = SP.select_layouts(lay, sc.cmax, sc.shares)
+    assert [len(l.slots) for l in L] == [1, 2, 2] and not L[0].mig and L[1].mig and L[2].mig
+    assert len({s.dom for s in L[2].slots}) == 2 and len({s.dom for s in L[1].slots}) == 1
+    with pytest.raises(ValueError):
+        SP.select_layouts([[(400, 8, 0), (300, 8, 1)]], 2, sc.shares)  # 16 memory eighths
+    pool = synth.make_pool(27)
+    Q = synth.table_v_windows(pool)[:6]
+    cost = {}
+    for name, (scfg, lay) in synth.BASELINE_SPACES.items():
+        L = SP.select_layouts(lay, scfg.cmax, scfg.shares) if lay else None
+        sp = SP.build_space(scfg.window, scfg.cmax, scfg.shares, scfg.mig, layouts=L)
+        cost[name] = [BR.dp_opt(sp, [int(x) for x in w], pool) for w in Q]
+    for i in range(len(Q)):
+        solo = cost["mig_mps"][i]["solo"]
+        assert all(cost[n][i]["solo"] == solo for n in cost)
+        assert cost["mig_mps"][i]["cost"] <= cost["mps_only"][i]["cost"] <= solo
+        assert cost["mig_mps"][i]["cost"] <= cost["mig_only"][i]["cost"] <= solo
+        # MIG-only job sets have at most 2 members
+        rgs = cost["mig_only"][i]["rgs"]
+        assert max(rgs.count(b) for b in set(rgs)) <= 2
