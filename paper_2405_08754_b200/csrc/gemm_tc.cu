@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -225,6 +226,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, tensormap prefetch, TMEM
+  // allocation) overlaps the tail of the previous kernel on the stream; no operand, bias or
+  // mask is read before the previous grid has completed and flushed its writes.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) TRACE(1);
 
   if (warp == 0) {
@@ -288,6 +293,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
     }
     mbar_wait(acc_bar, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    // the main loop is done: let the next kernel on the stream start its prologue (it still
+    // waits for this grid's completion before reading what the epilogue writes)
+    asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x == 128) TRACE(194);
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
     // the stage buffers are idle now: per-warp 32 x 33 transpose tile
@@ -451,6 +459,11 @@ __global__ void reduce_splits_kernel(int S, int64_t n, int N1, const float* __re
 }
 
 thread_local std::string g_tc_err;
+// programmatic dependent launch of the GEMMs (HRP_NO_PDL=1 disables it, for A/B timing)
+const bool g_pdl = [] {
+  const char* s = getenv("HRP_NO_PDL");
+  return !(s && s[0] == '1');
+}();
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 bool get_encode() {
@@ -505,8 +518,18 @@ hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
     attr = true;
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, splits);
-  tc_gemm_kernel<BN, STAGES, EPI><<<grid, kThreadsTc, smem, st>>>(ma0, ma1, mb0, mb1, a);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES, EPI>, ma0, ma1, mb0, mb1, a);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
 }
