@@ -422,7 +422,7 @@ def run_gpu(args, cfg):
                "clocks": clk,
                "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
         rl = rooflines(prof, args.steps, evals_k, cfg, osp)
-        res["roofline"] = dominant(rl)
+        res["roofline"] = dominant(rl, args.config)
         tot = sum(v["ms_per_step"] for v in rl.values())
         res["roofline"]["share_of_step"] = rl[res["roofline"]["kernel"]]["ms_per_step"] / tot
         res["rooflines"] = rl
@@ -535,20 +535,23 @@ def rooflines(prof, steps, evals, cfg, osp):
     return out
 
 
-def measured_traffic(cls):
+def measured_traffic(cls, cfgk=2):
     """DRAM bytes per launch of kernel class `cls` from the committed ncu launch list of this
-    bench command (profiles/traffic.json, written by tools/traffic_from_launches.py), or None."""
+    bench command (profiles/traffic.json for config 2 and the brute force of config 3,
+    profiles/traffic_cfg<k>.json otherwise; written by tools/traffic_from_launches.py), or
+    None when no launch list of that configuration is committed."""
+    fn = "traffic.json" if cfgk in (2, 3) else f"traffic_cfg{cfgk}.json"
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", fn)))
         return t["classes"][cls]["dram_bytes_per_launch"], t["source"]
     except Exception:
         return None, None
 
 
-def dominant(rl):
+def dominant(rl, cfgk=2):
     name = max(rl, key=lambda k: rl[k]["ms_per_step"])
     r = rl[name]
-    traffic, src = measured_traffic(name)
+    traffic, src = measured_traffic(name, cfgk)
     return {"kernel": name, "bound": r.get("bound"), "achieved": r.get("achieved"),
             "peak": r.get("peak"), "unit": r.get("unit"), "frac": r.get("frac"),
             "traffic": traffic, "traffic_src": src, "peak_src": r.get("peak_src"),
