@@ -84,3 +84,20 @@ def test_kernel_classes_match_header():
     assert ids["COUNT"] == len(hrp.KERNEL_CLASSES)
     assert ids["HEAD_BWD"] == hrp.KERNEL_CLASSES.index("head_bwd")
     assert ids["GEMM_BWD"] == hrp.KERNEL_CLASSES.index("gemm_bwd")
+
+
+def test_measured_traffic_is_per_configuration():
+    # the roofline's `traffic` comes from a launch list of the same configuration only
+    t2, src2 = bench.measured_traffic("gemm_fwd", 2)
+    t4, src4 = bench.measured_traffic("gemm_fwd", 4)
+    assert t2 and "cfg2" in src2 and t4 and "cfg4" in src4 and t4 > 10 * t2
+    assert bench.measured_traffic("gemm_fwd", 1) == (None, None)   # no cfg1 list committed
+    tb, srcb = bench.measured_traffic("brute", 3)
+    assert tb and "brute" in srcb
+
+
+def test_clock_sampler_without_gpu():
+    # no NVML device and no nvidia-smi here: the sampler must not raise, and reports None
+    c = bench.Clocks(0)
+    out = c.stop()
+    assert out is None or {"sm_mhz", "sm_max_mhz", "reasons", "samples"} <= set(out)
