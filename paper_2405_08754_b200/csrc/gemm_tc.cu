@@ -459,6 +459,11 @@ __global__ void reduce_splits_kernel(int S, int64_t n, int N1, const float* __re
 }
 
 thread_local std::string g_tc_err;
+// diagnostics: HRP_WGRAD_DIV=d divides the one-wave split-K count by d (A/B timing only)
+const int g_wgrad_div = [] {
+  const char* s = getenv("HRP_WGRAD_DIV");
+  return s ? atoi(s) : 1;
+}();
 // programmatic dependent launch of the GEMMs (HRP_NO_PDL=1 disables it, for A/B timing)
 const bool g_pdl = [] {
   const char* s = getenv("HRP_NO_PDL");
@@ -602,6 +607,7 @@ hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes
   // one wave: tiles x S <= SMs (each CTA holds one SM; a second partial wave costs a whole CTA
   // time for a few tiles, and every extra split adds an M x N partial to the reduction)
   int S = (int)std::max(1L, std::min(64L, (long)g->nsm / tiles));
+  if (g_wgrad_div > 1) S = std::max(1, S / g_wgrad_div);  // diagnostics: fewer, longer splits
   int kc = (K + S - 1) / S;
   kc = (kc + BK - 1) / BK * BK;
   S = (K + kc - 1) / kc;
