@@ -1050,14 +1050,12 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   const int H = c->hs.head_width();
   hrp_status s;
   prof_begin(c);
-  // one thread per sample, 32 per block: the per-sample decode is latency-bound, spread it
-  sample_kernel<<<(B + 31) / 32, 32, 0, c->stream>>>(
-      c->dt.sp, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r, c->rep_done,
-      c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx);
-  if ((s = launch_check(c, HRP_K_SAMPLE))) return s;
-  prof_begin(c);
-  encode_kernel<<<(2 * B + 7) / 8, 256, 0, c->stream>>>(2 * B, c->hs.W, c->bwin, c->bsched,
-                                                         c->dt.pool, c->X.hi, c->X.lo, c->ldX);
+  // replay sample + encoding of s and s' in one launch, one warp per sample (the per-sample
+  // decode is latency-bound: 8 samples per 256-thread CTA spreads it over the SMs)
+  sample_encode_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(
+      c->dt.sp, c->dt.pool, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r,
+      c->rep_done, c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx, c->X.hi, c->X.lo,
+      c->ldX);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
   const bool tcb = tc_mode(c);
   if (tcb && (s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->ldX, c->X, c->XT, c->Bp)))

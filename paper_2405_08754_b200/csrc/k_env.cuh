@@ -1,6 +1,6 @@
 // Environment-side kernels of libhrp (sm_100a):
 //   encode_kernel      a2  state encoding (Table VI; reading R10)
-//   sample_kernel      a8  replay sampling
+//   sample_encode_kernel  a8 + a2 replay sampling fused with the encoding of s and s'
 // plus the device helpers of the selection / TD kernels (k_select.cuh): co-run time (a6),
 // valid-action count, permutation order, and their argument blocks.
 //   sgd_kernel         a13 SGD + target sync
@@ -13,52 +13,70 @@ namespace hrp {
 // a2: x[row] = W rows of [features(12) | c/cbar, m/mbar, T/Tbar | scheduled | U/W]
 // One warp per state.
 // X is written raw, or (Xlo != NULL) split into tf32 hi / lo planes for the tensor-core GEMMs.
+
+// Window means as the reciprocal scales W / sum (the ratios of P:240 / R10), warp-wide.
+__device__ __forceinline__ void window_scales(int W, const uint8_t* __restrict__ w,
+                                              const DevPool& pool, float& ic, float& im,
+                                              float& iT) {
+  const int lane = threadIdx.x & 31;
+  int64_t sc = 0, sm = 0, sT = 0;
+  for (int j = lane; j < W; j += 32) {
+    int p = w[j];
+    sc += pool.c[p];
+    sm += pool.m[p];
+    sT += pool.T[p];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    sT += __shfl_xor_sync(0xffffffffu, sT, o);
+  }
+  const float fW = (float)W;
+  ic = fW / (float)sc;
+  im = fW / (float)sm;
+  iT = fW / (float)sT;
+}
+
+// One state's row of X (warp-wide) from its window, scheduled mask and window scales.
+__device__ __forceinline__ void encode_row(int W, const uint8_t* __restrict__ w, uint64_t s,
+                                           float ic, float im, float iT, const DevPool& pool,
+                                           float* __restrict__ x, float* __restrict__ xl) {
+  const int lane = threadIdx.x & 31;
+  const int in = W * 17;
+  const int U = W - __popcll(s);
+  const float fW = (float)W;
+#pragma unroll 4
+  for (int i = lane; i < in; i += 32) {   // unrolled: 4 independent load chains in flight
+    const int j = i / 17, col = i - j * 17;
+    const int p = w[j];
+    float v;
+    if (col < 12) v = pool.feat[p * 12 + col];
+    else if (col == 12) v = (float)pool.c[p] * ic;
+    else if (col == 13) v = (float)pool.m[p] * im;
+    else if (col == 14) v = (float)pool.T[p] * iT;
+    else if (col == 15) v = (float)((s >> j) & 1ull);
+    else v = (float)U / fW;
+    if (xl) {
+      const float h = tf32_rna(v);
+      x[i] = h;
+      xl[i] = v - h;
+    } else {
+      x[i] = v;
+    }
+  }
+}
+
 __global__ void encode_kernel(int M, int W, const uint8_t* __restrict__ win,
                               const uint64_t* __restrict__ sched, DevPool pool,
                               float* __restrict__ X, float* __restrict__ Xlo, int ldx) {
   const int warps = blockDim.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int in = W * 17;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
     const uint8_t* w = win + (size_t)row * W;
-    int64_t sc = 0, sm = 0, sT = 0;
-    for (int j = lane; j < W; j += 32) {
-      int p = w[j];
-      sc += pool.c[p];
-      sm += pool.m[p];
-      sT += pool.T[p];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sc += __shfl_xor_sync(0xffffffffu, sc, o);
-      sm += __shfl_xor_sync(0xffffffffu, sm, o);
-      sT += __shfl_xor_sync(0xffffffffu, sT, o);
-    }
-    const uint64_t s = sched[row];
-    const int U = W - __popcll(s);
-    const float fW = (float)W;
-    const float ic = fW / (float)sc, im = fW / (float)sm, iT = fW / (float)sT;
-    float* x = X + (size_t)row * ldx;
-    float* xl = Xlo ? Xlo + (size_t)row * ldx : nullptr;
-#pragma unroll 4
-    for (int i = lane; i < in; i += 32) {   // unrolled: 4 independent load chains in flight
-      const int j = i / 17, col = i - j * 17;
-      const int p = w[j];
-      float v;
-      if (col < 12) v = pool.feat[p * 12 + col];
-      else if (col == 12) v = (float)pool.c[p] * ic;
-      else if (col == 13) v = (float)pool.m[p] * im;
-      else if (col == 14) v = (float)pool.T[p] * iT;
-      else if (col == 15) v = (float)((s >> j) & 1ull);
-      else v = (float)U / fW;
-      if (xl) {
-        const float h = tf32_rna(v);
-        x[i] = h;
-        xl[i] = v - h;
-      } else {
-        x[i] = v;
-      }
-    }
+    float ic, im, iT;
+    window_scales(W, w, pool, ic, im, iT);
+    encode_row(W, w, sched[row], ic, im, iT, pool, X + (size_t)row * ldx,
+               Xlo ? Xlo + (size_t)row * ldx : nullptr);
   }
 }
 
@@ -176,36 +194,54 @@ struct SelArgs {
 };
 
 // ---------------------------------------------------------------------------------------
-// a8: replay sample.  idx_b = floor(u_b * n_filled / 2^32).  Writes the batch state twice
-// (rows [0,B) = s, rows [B,2B) = s') so that one encode + one GEMM pass covers both.
-__global__ void sample_kernel(DevSpace sp, int B, const uint32_t* __restrict__ u, int64_t n_filled,
-                              const uint8_t* __restrict__ rep_win, const uint64_t* __restrict__ rep_sched,
-                              const int64_t* __restrict__ rep_act, const float* __restrict__ rep_r,
-                              const uint8_t* __restrict__ rep_done, uint8_t* __restrict__ bwin,
-                              uint64_t* __restrict__ bsched, int64_t* __restrict__ bact,
-                              float* __restrict__ br, uint8_t* __restrict__ bdone,
-                              int64_t* __restrict__ out_idx) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  const int64_t idx = (int64_t)(((uint64_t)u[b] * (uint64_t)n_filled) >> 32);
+// a8 + a2 fused for the update: one warp per replay sample b draws
+// idx_b = floor(u_b * n_filled / 2^32), gathers the transition into the batch buffers and encodes both of its states -- row b
+// (s: window, scheduled mask) and row B + b (s': the same window with the action's jobs
+// scheduled) -- sharing the window scales.  Same arithmetic as encode_kernel over the 2B rows;
+// one launch and one pass over the window.
+__global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restrict__ u,
+                                     int64_t n_filled, const uint8_t* __restrict__ rep_win,
+                                     const uint64_t* __restrict__ rep_sched,
+                                     const int64_t* __restrict__ rep_act,
+                                     const float* __restrict__ rep_r,
+                                     const uint8_t* __restrict__ rep_done, uint8_t* __restrict__ bwin,
+                                     uint64_t* __restrict__ bsched, int64_t* __restrict__ bact,
+                                     float* __restrict__ br, uint8_t* __restrict__ bdone,
+                                     int64_t* __restrict__ out_idx, float* __restrict__ X,
+                                     float* __restrict__ Xlo, int ldx) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int W = sp.W;
-  for (int j = 0; j < W; ++j) {
-    const uint8_t v = rep_win[idx * W + j];
-    bwin[(size_t)b * W + j] = v;
-    bwin[(size_t)(B + b) * W + j] = v;
+  for (int b = blockIdx.x * warps + (threadIdx.x >> 5); b < B; b += gridDim.x * warps) {
+    const int64_t idx = (int64_t)(((uint64_t)u[b] * (uint64_t)n_filled) >> 32);
+    const uint8_t* w = rep_win + idx * W;
+    const uint64_t s = rep_sched[idx];
+    uint64_t gm = 0;
+    if (lane == 0) {
+      const int64_t a = rep_act[idx];
+      int g[4], sg[4];
+      const int l = decode_action(sp, a, g, sg);
+      for (int i = 0; i < sp.lay_n[l]; ++i) gm |= 1ull << g[i];
+      bsched[b] = s;
+      bsched[B + b] = s | gm;
+      bact[b] = a;
+      br[b] = rep_r[idx];
+      bdone[b] = rep_done[idx];
+      if (out_idx) out_idx[b] = idx;
+    }
+    gm = __shfl_sync(0xffffffffu, gm, 0);
+    for (int j = lane; j < W; j += 32) {
+      const uint8_t v = w[j];
+      bwin[(size_t)b * W + j] = v;
+      bwin[(size_t)(B + b) * W + j] = v;
+    }
+    float ic, im, iT;
+    window_scales(W, w, pool, ic, im, iT);
+    encode_row(W, w, s, ic, im, iT, pool, X + (size_t)b * ldx,
+               Xlo ? Xlo + (size_t)b * ldx : nullptr);
+    encode_row(W, w, s | gm, ic, im, iT, pool, X + (size_t)(B + b) * ldx,
+               Xlo ? Xlo + (size_t)(B + b) * ldx : nullptr);
   }
-  const int64_t a = rep_act[idx];
-  int g[4], sg[4];
-  const int l = decode_action(sp, a, g, sg);
-  uint64_t gm = 0;
-  for (int i = 0; i < sp.lay_n[l]; ++i) gm |= 1ull << g[i];
-  const uint64_t s = rep_sched[idx];
-  bsched[b] = s;
-  bsched[B + b] = s | gm;
-  bact[b] = a;
-  br[b] = rep_r[idx];
-  bdone[b] = rep_done[idx];
-  if (out_idx) out_idx[b] = idx;
 }
 
 struct TdArgs {
