@@ -826,7 +826,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(cudaMemsetAsync(c->sched, 0, sizeof(uint64_t) * E, c->stream));
   const size_t N = cfg->replay_capacity;
   CK(ar.alloc((void**)&c->rep_win, N * W));
-  CK(ar.alloc((void**)&c->rep_sched, N * 8));
+  CK(ar.alloc((void**)&c->rep_sched, N * 16));  // [N][2]: s and s' scheduled masks
   CK(ar.alloc((void**)&c->rep_act, N * 8));
   CK(ar.alloc((void**)&c->rep_r, N * 4));
   CK(ar.alloc((void**)&c->rep_done, N));

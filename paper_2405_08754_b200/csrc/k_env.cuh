@@ -183,7 +183,7 @@ struct SelArgs {
   float* qmax;              // INFER
   // replay
   uint8_t* rep_win;
-  uint64_t* rep_sched;
+  uint64_t* rep_sched;  // [N_rep][2]: scheduled mask of s and of s' (= s | the action's jobs)
   int64_t* rep_act;
   float* rep_r;
   uint8_t* rep_done;
@@ -195,10 +195,11 @@ struct SelArgs {
 
 // ---------------------------------------------------------------------------------------
 // a8 + a2 fused for the update: one warp per replay sample b draws
-// idx_b = floor(u_b * n_filled / 2^32), gathers the transition into the batch buffers and encodes both of its states -- row b
-// (s: window, scheduled mask) and row B + b (s': the same window with the action's jobs
-// scheduled) -- sharing the window scales.  Same arithmetic as encode_kernel over the 2B rows;
-// one launch and one pass over the window.
+// idx_b = floor(u_b * n_filled / 2^32), gathers the transition into the batch buffers and
+// encodes both of its states -- row b (s: window, scheduled mask) and row B + b (s': the same
+// window with the action's jobs scheduled; the select kernel stores that mask beside s at
+// insert time) -- sharing the window scales.  Same arithmetic as encode_kernel over the 2B
+// rows; one launch and one pass over the window.
 __global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restrict__ u,
                                      int64_t n_filled, const uint8_t* __restrict__ rep_win,
                                      const uint64_t* __restrict__ rep_sched,
@@ -215,21 +216,15 @@ __global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uin
   for (int b = blockIdx.x * warps + (threadIdx.x >> 5); b < B; b += gridDim.x * warps) {
     const int64_t idx = (int64_t)(((uint64_t)u[b] * (uint64_t)n_filled) >> 32);
     const uint8_t* w = rep_win + idx * W;
-    const uint64_t s = rep_sched[idx];
-    uint64_t gm = 0;
+    const uint64_t s = rep_sched[2 * idx], s2 = rep_sched[2 * idx + 1];
     if (lane == 0) {
-      const int64_t a = rep_act[idx];
-      int g[4], sg[4];
-      const int l = decode_action(sp, a, g, sg);
-      for (int i = 0; i < sp.lay_n[l]; ++i) gm |= 1ull << g[i];
       bsched[b] = s;
-      bsched[B + b] = s | gm;
-      bact[b] = a;
+      bsched[B + b] = s2;
+      bact[b] = rep_act[idx];
       br[b] = rep_r[idx];
       bdone[b] = rep_done[idx];
       if (out_idx) out_idx[b] = idx;
     }
-    gm = __shfl_sync(0xffffffffu, gm, 0);
     for (int j = lane; j < W; j += 32) {
       const uint8_t v = w[j];
       bwin[(size_t)b * W + j] = v;
@@ -239,7 +234,7 @@ __global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uin
     window_scales(W, w, pool, ic, im, iT);
     encode_row(W, w, s, ic, im, iT, pool, X + (size_t)b * ldx,
                Xlo ? Xlo + (size_t)b * ldx : nullptr);
-    encode_row(W, w, s | gm, ic, im, iT, pool, X + (size_t)(B + b) * ldx,
+    encode_row(W, w, s2, ic, im, iT, pool, X + (size_t)(B + b) * ldx,
                Xlo ? Xlo + (size_t)(B + b) * ldx : nullptr);
   }
 }

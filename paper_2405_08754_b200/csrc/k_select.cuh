@@ -755,7 +755,8 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
       const uint64_t s2 = sched | gm;
       d = s2 == all;
       slot = (a.t_step * (int64_t)a.M + row) % a.N_rep;
-      a.rep_sched[slot] = sched;
+      a.rep_sched[2 * slot] = sched;       // s
+      a.rep_sched[2 * slot + 1] = s2;      // s' (the action's jobs scheduled)
       a.rep_act[slot] = act;
       a.rep_r[slot] = (float)r;
       a.rep_done[slot] = (uint8_t)d;
