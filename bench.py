@@ -129,8 +129,9 @@ def run_reference(args, cfg):
 class Clocks:
     """SM clock + throttle-reason sampling DURING the timed region (B200_PROFILING.md clocks
     line). A timed region here is ~10 ms of GPU work, shorter than nvidia-smi's 100 ms
-    sampling period, so NVML is polled from a thread every ~0.5 ms while the host waits on
-    the stream; one sample is always taken at stop(). Falls back to nvidia-smi if NVML is
+    sampling period, so NVML is polled from a thread every ~5 ms while the host waits on the
+    stream (a 0.5 ms period perturbed the GPU: cfg 3 ran 42-57 k instead of 80 k windows/s,
+    profiles/r1zp_cfg3_nvml_period.txt); one sample is always taken at stop(). Falls back to nvidia-smi if NVML is
     unavailable."""
 
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
@@ -179,7 +180,7 @@ class Clocks:
                 self._sample()
             except Exception:
                 return
-            time.sleep(0.0005)
+            time.sleep(0.005)   # NVML queries every 0.5 ms slowed the brute-force kernel (r1zp)
 
     def _smi(self, dev):
         self.path = f"/tmp/hrp_clocks_{os.getpid()}.csv"
