@@ -446,8 +446,17 @@ __global__ void reduce_splits_kernel(int S, int64_t n, int N1, const float* __re
                                      float* __restrict__ out, float* __restrict__ db) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    // all S partial loads in flight before the (fixed-order, deterministic) adds
     float s = 0.f;
-    for (int z = 0; z < S; ++z) s += ws[(size_t)z * n + i];
+    int z = 0;
+    for (; z + 8 <= S; z += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcs(ws + (size_t)(z + k) * n + i);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += v[k];
+    }
+    for (; z < S; ++z) s += __ldcs(ws + (size_t)z * n + i);
     if (db == nullptr) {
       out[i] = s;
     } else {
