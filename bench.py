@@ -244,8 +244,7 @@ def run_gpu(args, cfg):
     E, B = cfg.n_envs, cfg.batch
     with torch.cuda.stream(stream):
         sess = Session(cfg, pool, init_weights=th, device=local, rank=rank, world=world,
-                       nccl_id=nccl_id, argmax_mode=args.argmax, gemm_mode=args.gemm,
-                       stream=stream)
+                       nccl_id=nccl_id, argmax_mode=args.argmax, stream=stream)
         sess.reset(synth.make_windows(pool, E, sc.window, rank=rank,
                                        first_env=parallel.env_shard(E, rank)))
     total = args.warmup + args.steps
@@ -405,7 +404,7 @@ def run_gpu(args, cfg):
                "config": {"workload": workload_name(cfg), "global_envs": world * E,
                           "actions_per_state": int(sess_actions(osp)),
                           "argmax": "explicit" if sess_explicit(args, sc) else "pruned-exact",
-                          "gemm": {0: "auto", 1: "fp32 CUDA-core", 2: "tcgen05 3xTF32"}[args.gemm],
+                          "gemm": "tcgen05 3xTF32 (fp32-accurate), TMA + TMEM",
                           "l2": "flushed (256 MiB memset) between timed steps",
                           "launch": "CUDA graph per step (captured before the timed region)"
                                     if args.graph else "eager stream launches",
@@ -451,7 +450,7 @@ def sess_actions(osp):
 
 
 def sess_explicit(args, sc):
-    return args.argmax == 1 or (args.argmax == 0 and sc.window <= 16)
+    return args.argmax == 1       # auto = the exact pruned search (hrp.h argmax_mode)
 
 
 def _peaks():
@@ -762,7 +761,6 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--argmax", type=int, default=0, help="0 auto, 1 explicit, 2 pruned")
-    ap.add_argument("--gemm", type=int, default=0, help="0 auto, 1 CUDA-core fp32, 2 tcgen05")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the timed steps eagerly instead of from per-step CUDA graphs")

@@ -38,7 +38,8 @@ typedef enum {
   HRP_ECUDA = 3,  /* CUDA runtime error (message has the CUDA error string)         */
   HRP_ENCCL = 4,  /* NCCL error                                                     */
   HRP_ERANGE = 5, /* size outside the supported range (W, Cmax, P, n, ...)          */
-  HRP_ESTATE = 6  /* call not valid in the current state (e.g. replay < batch)      */
+  HRP_ESTATE = 6, /* call not valid in the current state (e.g. replay < batch)      */
+  HRP_ENUMERIC = 7 /* non-finite Q values met by a greedy argmax (from hrp_sync)     */
 } hrp_status;
 
 typedef struct hrp_ctx hrp_ctx; /* opaque: tables, weights, replay, workspaces, NCCL comm */
@@ -80,14 +81,16 @@ typedef struct {
 typedef struct {
   int32_t n_envs;           /* E: environments on this rank, >= 1                          */
   int32_t batch;            /* B: replay batch on this rank, >= 1                          */
-  int32_t replay_capacity;  /* N_rep >= batch                                              */
+  int32_t replay_capacity;  /* N_rep >= max(batch, n_envs) (one step's E inserts must land  */
+                            /* in distinct ring slots)                                     */
   int32_t hidden_layers;    /* d >= 1 (Table VI: fully connected + ReLU)                   */
   int32_t hidden_width;     /* w, multiple of 4, <= 1024                                   */
   float gamma;              /* discount                                            */
   float lr;                 /* SGD learning rate alpha                             */
   float reward_lambda;      /* r = r_f + lambda * sum r_i (Table VI, R9)                   */
-  int32_t argmax_mode;      /* 0 auto, 1 explicit enumeration of every action, 2 pruned  */
-  int32_t gemm_mode;        /* 0 auto, 1 fp32 CUDA-core GEMM, 2 tcgen05 3xTF32 GEMM        */
+  int32_t argmax_mode;      /* 0 auto (= 2), 1 explicit enumeration of every valid action  */
+                            /* (W <= 16), 2 exact top-C pruned search; same actions bit    */
+                            /* for bit (R15)                                    */
 } hrp_train_cfg;
 
 /* ---- lifecycle ------------------------------------------------------------------------ */
@@ -145,6 +148,17 @@ hrp_status hrp_q_forward(hrp_ctx *ctx, int64_t n, const uint8_t *d_windows,
 hrp_status hrp_dqn_update(hrp_ctx *ctx, const uint32_t *d_u_replay, int sync_target,
                           float *d_loss, int64_t *d_sample_idx, int64_t *d_astar);
 
+/* Data-parallel building blocks of hrp_dqn_update:
+ * hrp_dqn_grad runs the same update up to the backward and writes this rank's gradient of the
+ * loss -- sum over its B samples of dL/dtheta, already scaled by 1 / (B * world) -- to d_grad
+ * (device f32 [hrp_n_params], caller-owned) WITHOUT the NCCL allreduce and without changing the
+ * weights; hrp_apply_grad then performs the SGD step theta -= lr * d_grad (+ target sync) with
+ * any gradient, e.g. one summed over shards by the caller.  hrp_dqn_update == hrp_dqn_grad +
+ * allreduce + hrp_apply_grad.  Same errors as hrp_dqn_update. */
+hrp_status hrp_dqn_grad(hrp_ctx *ctx, const uint32_t *d_u_replay, float *d_loss,
+                        int64_t *d_sample_idx, int64_t *d_astar, float *d_grad);
+hrp_status hrp_apply_grad(hrp_ctx *ctx, const float *d_grad, int sync_target);
+
 /* ---- exhaustive optimum ------------------------------ */
 
 /* For each of n windows (uint8 [n][W], W <= 12): the minimum over set partitions of Q into
@@ -153,11 +167,25 @@ hrp_status hrp_dqn_update(hrp_ctx *ctx, const uint32_t *d_u_replay, int sync_tar
  * set's partitioning ties to the lowest action index.  Outputs (device): d_best_corun int64
  * [n] (the optimum), d_solo int64 [n] (time sharing), d_rgs uint8 [n][W] (job set of each
  * window position, sets numbered by their smallest position), d_block_action int64 [n][W]
- * (action index of each job set in set order, -1 padded).  Stateless; stream may be NULL. */
+ * (action index of each job set in set order, -1 padded).  Stateless and synchronous (returns
+ * once the results are written); stream may be NULL. */
 hrp_status hrp_bruteforce_optimum(const hrp_space *space, const hrp_profiles *profiles,
                                   int64_t n_windows, const uint8_t *d_windows,
                                   int64_t *d_best_corun, int64_t *d_solo, uint8_t *d_rgs,
                                   int64_t *d_block_action, void *cuda_stream);
+
+/* The same search with the layout space's tables kept resident: hrp_brute_create validates
+ * and uploads them once (synchronous; errors as hrp_bruteforce_optimum), hrp_brute_run only
+ * enqueues the search kernel on `cuda_stream` (asynchronous, no allocation, graph-capturable),
+ * hrp_brute_destroy frees the tables (after the caller's work on them is complete).
+ * hrp_bruteforce_optimum = create + run + synchronize + destroy. */
+typedef struct hrp_brute hrp_brute;
+hrp_status hrp_brute_create(const hrp_space *space, const hrp_profiles *profiles, int device,
+                            void *cuda_stream, hrp_brute **out);
+hrp_status hrp_brute_run(hrp_brute *plan, int64_t n_windows, const uint8_t *d_windows,
+                         int64_t *d_best_corun, int64_t *d_solo, uint8_t *d_rgs,
+                         int64_t *d_block_action, void *cuda_stream);
+hrp_status hrp_brute_destroy(hrp_brute *plan);
 
 /* ---- host helpers (no device work) ---------------------------------------------------- */
 
@@ -216,7 +244,9 @@ hrp_status hrp_eval_counts(hrp_ctx *ctx, int64_t *out);
 hrp_status hrp_diag_gemm(int device, void *cuda_stream, int M, int N, int K, const float *d_A,
                          const float *d_W, const float *d_bias, float *d_D,
                          uint64_t *d_trace, int reps, int force_bn, float *ms_out);
-/* Block until the context's stream is idle; returns any pending CUDA/NCCL error. */
+/* Block until the context's stream is idle; returns any pending CUDA/NCCL error, or
+ * HRP_ENUMERIC (once, then cleared) if a greedy argmax since the last call met non-finite Q
+ * values (e.g. diverged weights); such a state took its lowest valid action instead. */
 hrp_status hrp_sync(hrp_ctx *ctx);
 const char *hrp_last_error(void);
 const char *hrp_version(void);

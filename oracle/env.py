@@ -24,11 +24,13 @@ case of the Q-update rule; gamma = 0 / done -> y = r.
 from __future__ import annotations
 
 import itertools
+import multiprocessing as mp
 
 import numpy as np
 
 from . import actions as A
 from . import corun as CR
+from . import pruned as PR
 from . import qnet as QN
 
 NEAR_TIE = 1e-4  # reading R15: argmax mismatch allowed iff oracle gap <= 1e-4 max(1, |Q|)
@@ -107,13 +109,44 @@ def greedy_explicit(tab: Tables, Fv, FcL, FcJ, sched: int):
     return best_idx, best
 
 
+# -- all-core mode: the per-state argmax (the oracle's dominant cost) mapped over worker
+# processes.  Each state's argmax is independent of every other, so this only changes where
+# the same function runs, not what it computes.
+_WORKER = {}
+
+
+def _worker_init(space, argmax):
+    if argmax == "pruned":
+        off = A.offsets(space)
+        _WORKER["fn"] = lambda Fv, FcL, FcJ, s: PR.greedy_pruned(space, Fv, FcL, FcJ, s, off)
+    else:
+        tab = Tables(space)
+        _WORKER["fn"] = lambda Fv, FcL, FcJ, s: greedy_explicit(tab, Fv, FcL, FcJ, s)
+
+
+def _worker_call(item):
+    return _WORKER["fn"](*item)
+
+
 class OracleDQN:
-    """The vectorised DQN environment + agent of SURVEY §8(c) Q1-Q4, one rank."""
+    """The vectorised DQN environment + agent of SURVEY §8(c) Q1-Q4, one rank.
+
+    argmax: "explicit" (every valid action, env.greedy_explicit) or "pruned" (the exact top-C
+    search of oracle/pruned.py, same result); workers > 1 maps the per-state argmax over that
+    many processes (all-core mode; results are identical)."""
 
     def __init__(self, space, pool, net, theta0, n_envs, batch, replay_capacity,
-                 gamma=0.99, lr=1e-3, reward_lambda=0.0, q3=1, greedy=None):
+                 gamma=0.99, lr=1e-3, reward_lambda=0.0, q3=1, greedy=None, argmax="explicit",
+                 workers=0):
         self.sp = space
         self.pool = pool
+        self.argmax = argmax
+        self.workers = workers
+        self._procs = None
+        if greedy is None and argmax == "pruned":
+            off = A.offsets(space)
+            greedy = lambda Fv, FcL, FcJ, s: PR.greedy_pruned(space, Fv, FcL, FcJ, s, off)
+        self.custom_greedy = greedy is not None
         self.tab = Tables(space) if greedy is None else None
         self.greedy_fn = greedy or (lambda Fv, FcL, FcJ, sched:
                                     greedy_explicit(self.tab, Fv, FcL, FcJ, sched))
@@ -132,9 +165,33 @@ class OracleDQN:
         self.rep_done = np.zeros(self.N, np.uint8)
         self.inserted = 0
         self.t = 0
-        self.near_ties = 0
+        self.near_ties = 0       # GPU argmax adopted under R15 (oracle gap within the window)
+        self.near_tie_gap = 0.0  # largest adopted gap, in units of max(1, |Q|)
+        self.greedy_calls = 0    # greedy argmaxes taken (the population near_ties is out of)
 
     # -- helpers -----------------------------------------------------------------------
+    def close(self):
+        if self._procs is not None:
+            self._procs.terminate()
+            self._procs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _greedy_many(self, items):
+        """[(Fv, FcL, FcJ, sched)] -> [(idx, Q^max)], in order."""
+        self.greedy_calls += len(items)
+        if self.workers > 1 and not self.custom_greedy and len(items) > 1:
+            if self._procs is None:
+                ctx = mp.get_context("spawn")
+                self._procs = ctx.Pool(self.workers, _worker_init, (self.sp, self.argmax))
+            ch = max(1, len(items) // (4 * self.workers))
+            return self._procs.map(_worker_call, items, chunksize=ch)
+        return [self.greedy_fn(*it) for it in items]
+
     def _heads(self, theta, windows, scheds):
         X = np.stack([encode(w, int(s), self.pool, self.sp.W) for w, s in zip(windows, scheds)])
         z, acts = QN.forward(theta, self.dims, X)
@@ -150,8 +207,10 @@ class OracleDQN:
             raise AssertionError(f"GPU chose invalid action {theirs}")
         qt = QN.q_fixed(Fv, FcL, FcJ, self.sp, l, g, sg)
         gap = (qmax - qt) / 4294967296.0
-        if gap <= NEAR_TIE * max(1.0, abs(qmax / 4294967296.0)):
+        rel = gap / max(1.0, abs(qmax / 4294967296.0))
+        if rel <= NEAR_TIE:
             self.near_ties += 1
+            self.near_tie_gap = max(self.near_tie_gap, rel)
             return theirs, 1
         raise AssertionError(f"argmax mismatch: oracle {mine} gpu {theirs} gap {gap}")
 
@@ -163,9 +222,11 @@ class OracleDQN:
     def q_forward(self, windows, scheds, gpu_argmax=None):
         z, _ = self._heads(self.theta, windows, scheds)
         out_a, out_q = [], []
+        hf = [head_fixed(z[b], self.sp) for b in range(len(windows))]
+        res = self._greedy_many([(h[3], h[4], h[5], int(scheds[b])) for b, h in enumerate(hf)])
         for b in range(len(windows)):
-            v, cL, cJ, Fv, FcL, FcJ = head_fixed(z[b], self.sp)
-            a, q = self.greedy_fn(Fv, FcL, FcJ, int(scheds[b]))
+            v, cL, cJ, Fv, FcL, FcJ = hf[b]
+            a, q = res[b]
             if gpu_argmax is not None and a >= 0:
                 a, _ = self._adopt(a, gpu_argmax[b], Fv, FcL, FcJ, q, int(scheds[b]))
                 q = q_fixed_idx_any(self.sp, self.off, Fv, FcL, FcJ, a)
@@ -181,14 +242,18 @@ class OracleDQN:
         done = np.zeros(E, np.uint8)
         cor = np.zeros(E, np.int64)
         qsel = np.zeros(E)
+        hf = [head_fixed(z[e], sp) for e in range(E)]
+        greedy_e = [e for e in range(E) if not int(u_explore[e]) < int(thr)]
+        res = dict(zip(greedy_e, self._greedy_many(
+            [(hf[e][3], hf[e][4], hf[e][5], int(self.sched[e])) for e in greedy_e])))
         for e in range(E):
             sched = int(self.sched[e])
-            v, cL, cJ, Fv, FcL, FcJ = head_fixed(z[e], sp)
+            v, cL, cJ, Fv, FcL, FcJ = hf[e]
             if int(u_explore[e]) < int(thr):
                 nv = A.n_valid(sp, sched)
                 a = A.kth_valid(sp, sched, A.explore_k(int(u_action[e]), nv), self.off)
             else:
-                a, q = self.greedy_fn(Fv, FcL, FcJ, sched)
+                a, q = res[e]
                 if gpu_actions is not None:
                     a, _ = self._adopt(a, gpu_actions[e], Fv, FcL, FcJ, q, sched)
             l, g, sg = A.decode(sp, a, self.off)
@@ -240,10 +305,14 @@ class OracleDQN:
         y = np.zeros(B)
         q_sa = np.zeros(B)
         dz = np.zeros_like(z_s)
+        live = [b for b in range(B) if not dn[b]]
+        hf = {b: head_fixed(z_n[b], sp) for b in live}
+        res = dict(zip(live, self._greedy_many(
+            [(hf[b][3], hf[b][4], hf[b][5], int(sch2[b])) for b in live])))
         for b in range(B):
             if not dn[b]:
-                v, cL, cJ, Fv, FcL, FcJ = head_fixed(z_n[b], sp)
-                a2, q2 = self.greedy_fn(Fv, FcL, FcJ, int(sch2[b]))
+                v, cL, cJ, Fv, FcL, FcJ = hf[b]
+                a2, q2 = res[b]
                 if gpu_astar is not None:
                     a2, _ = self._adopt(a2, gpu_astar[b], Fv, FcL, FcJ, q2, int(sch2[b]))
                 astar[b] = a2

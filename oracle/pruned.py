@@ -48,11 +48,13 @@ def greedy_pruned(space, Fv, FcL, FcJ, sched: int, off=None):
         for js in itertools.product(*cand):
             if len(set(js)) < C:
                 continue
+            score = Fv + FcL[l] + sum(FcJ[js[k]][st[k]] for k in range(C))
+            if lbest is not None and score < lbest:
+                continue                              # the index only breaks ties
             g = tuple(sorted(js))
             sigma = tuple(js.index(gi) for gi in g)   # member i (job g_i) -> its slot
-            score = Fv + FcL[l] + sum(FcJ[js[k]][st[k]] for k in range(C))
             w = A.rank_comb(g, W) * factorial(C) + A.lehmer(sigma)
-            if lbest is None or score > lbest or (score == lbest and w < lidx):
+            if lbest is None or score > lbest or w < lidx:
                 lbest, lidx = score, w
         if lbest is not None and (best is None or lbest > best):
             best, bi = lbest, off[l] + lidx

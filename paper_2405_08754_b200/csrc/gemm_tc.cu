@@ -524,12 +524,15 @@ hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
       !make_map(&mb1, B.lo, a.N, a.K, a.ldb, a.boxB))
     return HRP_ECUDA;
   constexpr int smem = TcSmem<BN, STAGES>::TOTAL;
-  static bool attr = false;
-  if (!attr) {
+  // the attribute belongs to the device context: track it per device
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
-    attr = true;
+    attr[dev & 63] = true;
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, splits);
   cudaLaunchConfig_t cfg = {};

@@ -14,7 +14,6 @@
 #include "tables.h"
 #include "dev.cuh"
 
-#include "k_gemm_simt.cuh"
 #include "k_env.cuh"
 #include "k_brute.cuh"
 #include "k_select.cuh"
@@ -216,8 +215,8 @@ hrp_status upload_tables(const HostSpace& hs, const hrp_profiles* prof, bool com
 
 }  // namespace
 
-// An activation-like buffer: raw fp32 (hi only, SIMT path) or split into tf32 hi / lo planes
-// (tensor-core path: every GEMM operand is written split by its producer).
+// An activation-like buffer split into tf32 hi / lo planes (every GEMM operand is written split
+// by its producer; hi + lo is the fp32 value exactly).
 struct Pl {
   float* hi = nullptr;
   float* lo = nullptr;
@@ -236,12 +235,12 @@ struct hrp_ctx {
   std::vector<Pl> act_t;              // target-pass hidden outputs [B][w] (concurrent scratch)
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  bool allreduce = true;              // hrp_dqn_grad exports the local gradient instead
   hrp_train_cfg cfg{};
   HostSpace hs;
   DevTables dt;
   Arena ar;
   bool explicit_mode = true;
-  int gemm_mode = 1;
   // network
   std::vector<int> dims;     // layer widths: in, w.., H
   std::vector<int64_t> woff; // per layer offset of W in the flat params
@@ -254,7 +253,7 @@ struct hrp_ctx {
   // (soff) and W^T [fi][r4(fo)] planes (soffT)
   std::vector<int64_t> soff, soffT;
   int64_t sstride = 0;        // floats per split plane
-  int ldX = 0, ldz = 0;       // row strides of X and dz (multiples of 4 on the tensor-core path)
+  int ldX = 0;                // row stride of X (multiple of 4: TMA rows are 16-B aligned)
   size_t ws_splitk_elems = 0;
   // env state
   uint8_t* win = nullptr;
@@ -271,18 +270,14 @@ struct hrp_ctx {
   Pl X;                               // [rows][in]
   std::vector<Pl> act;                // hidden outputs [rows][w] per layer
   float* z = nullptr;                 // [rows][H]
-  float* zt = nullptr;                // [B][H]
-  Pl dz;                              // [B][H]
-  float *dh0 = nullptr, *dh1 = nullptr;  // [B][w] (SIMT backward ping-pong)
-  std::vector<Pl> dhs, dhTs;          // tensor-core backward: per hidden layer dH, dH^T
-  // transposed operands of the tensor-core backward (leading dimension Bp = B rounded up to 4,
-  // zero padding columns): X^T [in][Bp], hidden outputs^T [w][Bp], dz^T [H][Bp]
+  std::vector<Pl> dhs, dhTs;          // backward: per hidden layer dH, dH^T
+  // transposed operands of the backward (leading dimension Bp = B rounded up to 4, zero padding
+  // columns): X^T [in][Bp], hidden outputs^T [w][Bp]
   int Bp = 0;
-  Pl XT, dzT;
+  Pl XT;
   std::vector<Pl> actT;
-  // structured head backward (k_head.cuh; tensor-core path): td writes per-sample descriptors
-  // instead of the dense dz, the head's two backward GEMMs become gathers / scatters
-  bool head_struct = false;
+  // structured head backward (k_head.cuh): td writes per-sample descriptors instead of a dense
+  // dz, the head's two backward GEMMs become gathers / scatters
   int* hdesc = nullptr;               // [B][8]
   int* tdesc = nullptr;               // [B][8] (a* on s')
   double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
@@ -294,9 +289,9 @@ struct hrp_ctx {
   float* br = nullptr;
   uint8_t* bdone = nullptr;
   float* dsq = nullptr;
-  int64_t* tmp_i64 = nullptr;         // [rows]
   unsigned long long* n_evals = nullptr;
   unsigned* sched_ctr = nullptr;      // [4]: row schedulers of the select / TD kernels, tdq ticket
+  unsigned* dev_err = nullptr;        // [1]: bit 0 = a greedy argmax found no comparable Q (NaN)
   size_t p_smem = 0;   // warp-per-state selection / TD kernels
   int sel_variant = 0; // 0 pruned argmax, 1..4 explicit enumeration with Cmax = variant
   int p_grid = 0;
@@ -309,6 +304,35 @@ struct hrp_ctx {
   size_t ev_used = 0;
   cudaEvent_t ev_begin = nullptr;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_rec;
+
+  // Releases everything the context owns, also after a partial hrp_env_create.
+  ~hrp_ctx() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (side) cudaStreamSynchronize(side);
+    if (comm) ncclCommDestroy(comm);
+    if (tc) tc_gemm_destroy(tc);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    ar.release();
+  }
+};
+
+// Exhaustive-optimum plan: the layout space's tables resident on one device (hrp_brute_*).
+struct hrp_brute {
+  int device = 0;
+  HostSpace hs;
+  Arena ar;
+  DevTables dt;
+  size_t smem = 0;
+  int grid_max = 0, nb8 = 0, n_items = 0;
+  int b8v[kBruteMaxB8] = {0, 0, 0, 0};
+  ~hrp_brute() {
+    cudaSetDevice(device);
+    ar.release();
+  }
 };
 
 namespace {
@@ -369,45 +393,6 @@ hrp_status on_side(hrp_ctx* c, F&& f) {
 }
 bool concurrent(const hrp_ctx* c) { return c->side != nullptr && !c->prof; }
 
-// C = epi(A . B) with the SIMT kernel; split-K (EPI_STORE) when `splitk_out` is set.
-template <bool AK, bool BKc, int EPI>
-hrp_status sgemm(hrp_ctx* c, int M, int N, int K, const float* A, int lda, const float* B,
-                 int ldb, float* C, int ldc, const float* bias, const float* aux, int ldaux) {
-  const int64_t t128 = (int64_t)((M + 127) / 128) * ((N + 127) / 128);
-  if (EPI != EPI_STORE && t128 >= 2 * 148) {
-    dim3 grid((N + 127) / 128, (M + 127) / 128, 1);
-    prof_begin(c);
-    sgemm_kernel<128, 128, 8, 8, AK, BKc, EPI><<<grid, 256, 0, c->stream>>>(
-        M, N, K, A, lda, B, ldb, C, ldc, bias, aux, ldaux, K);
-    return launch_check(c, c->gemm_cls);
-  }
-  const int64_t t64 = (int64_t)((M + 63) / 64) * ((N + 63) / 64);
-  if (EPI != EPI_STORE) {
-    dim3 grid((N + 63) / 64, (M + 63) / 64, 1);
-    prof_begin(c);
-    sgemm_kernel<64, 64, 4, 4, AK, BKc, EPI><<<grid, 256, 0, c->stream>>>(
-        M, N, K, A, lda, B, ldb, C, ldc, bias, aux, ldaux, K);
-    return launch_check(c, c->gemm_cls);
-  }
-  // split-K into the workspace, then a deterministic reduce into C (ldc == N)
-  int S = (int)std::min<int64_t>(32, std::max<int64_t>(1, (2 * 148 + t64 - 1) / t64));
-  int kc = (K + S - 1) / S;
-  kc = (kc + 7) / 8 * 8;
-  S = (K + kc - 1) / kc;
-  if ((size_t)S * M * N > c->ws_splitk_elems) return fail(HRP_ENOMEM, "split-K workspace too small");
-  dim3 grid((N + 63) / 64, (M + 63) / 64, S);
-  prof_begin(c);
-  sgemm_kernel<64, 64, 4, 4, AK, BKc, EPI_STORE><<<grid, 256, 0, c->stream>>>(
-      M, N, K, A, lda, B, ldb, c->ws_splitk, N, bias, aux, ldaux, kc);
-  hrp_status s = launch_check(c, c->gemm_cls);
-  if (s) return s;
-  const int64_t n = (int64_t)M * N;
-  prof_begin(c);
-  splitk_reduce_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(
-      S, n, c->ws_splitk, C);
-  return launch_check(c, c->gemm_cls);
-}
-
 // 3xTF32 hi/lo splits of the online (and transposed online) or target weights.
 hrp_status split_weights(hrp_ctx* c, bool target) {
   if (!c->tc) return HRP_OK;
@@ -452,12 +437,10 @@ hrp_status transpose(hrp_ctx* c, int cls, int rows, int cols, int ld_src, Pl src
   return launch_check(c, cls);
 }
 
-bool tc_mode(const hrp_ctx* c) { return c->gemm_mode == 2 && c->tc; }
-
 // Forward of one network over M rows of X: hidden outputs to c->act (kept for the backward
 // pass), head output z_out [M][H] (raw).  With t_rows > 0 the first t_rows rows of every hidden
 // output are also stored transposed in c->actT (operands of the weight-gradient GEMMs).
-// Tensor-core path: X and the hidden outputs are hi/lo planes; SIMT path: raw (hi only).
+// X and the hidden outputs are tf32 hi/lo planes (every GEMM operand is written split).
 // head_from: the head layer runs on rows [head_from, M) only (its output rows keep their
 // offsets in z_out); head_from >= M skips it (the structured update needs the head only where
 // every action is scored).
@@ -471,9 +454,8 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out
   int ldh = c->ldX;
   for (int i = 0; i < nl; ++i) {
     const int fi = c->dims[i], fo = c->dims[i + 1];
-    const float* Wm = theta + c->woff[i];
-    const float* b = Wm + (int64_t)fi * fo;
-    const Pl out = (i == nl - 1) ? Pl{z_out, nullptr} : act[i];
+    const float* b = theta + c->woff[i] + (int64_t)fi * fo;
+    const Pl out = (i == nl - 1) ? Pl{z_out, nullptr} : act[i];   // z_out unused if skipped
     hrp_status s;
     if (i == nl - 1 && head_from > 0) {
       if (head_from >= M) return HRP_OK;
@@ -482,16 +464,10 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out
       return tc_run(c, HRP_K_GEMM_FWD, TC_EPI_BIAS, M - head_from, fo, fi, hs.c(), ldh, hi,
                     hi + c->sstride, b, nullptr, 0, Pl{z_out + (size_t)head_from * fo, nullptr});
     }
-    if (tc_mode(c)) {
-      const Pl outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : Pl{};
-      const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
-      s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h.c(),
-                 ldh, hi, hi + c->sstride, b, nullptr, 0, out, outT, t_rows);
-    } else if (i < nl - 1) {
-      s = sgemm<true, true, EPI_BIAS_RELU>(c, M, fo, fi, h.hi, ldh, Wm, fi, out.hi, fo, b, nullptr, 0);
-    } else {
-      s = sgemm<true, true, EPI_BIAS>(c, M, fo, fi, h.hi, ldh, Wm, fi, out.hi, fo, b, nullptr, 0);
-    }
+    const Pl outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : Pl{};
+    const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
+    s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h.c(),
+               ldh, hi, hi + c->sstride, b, nullptr, 0, out, outT, t_rows);
     if (s) return s;
     h = out;
     ldh = fo;
@@ -499,19 +475,35 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out
   return HRP_OK;
 }
 
+// a12: allreduce-sum of layer i's gradient bucket (its W and b, contiguous in the flat layout)
+// over the ranks, enqueued on the current stream right after the layer's weight gradient is
+// complete -- on the side stream during the backward, so it overlaps the data-gradient chain of
+// the layers below.  Every rank issues the buckets in the same order (head first).
+hrp_status allreduce_layer(hrp_ctx* c, int i) {
+  if (c->world <= 1 || !c->allreduce) return HRP_OK;
+  const int nl = (int)c->dims.size() - 1;
+  const int64_t o = c->woff[i];
+  const int64_t n = (i + 1 < nl ? c->woff[i + 1] : c->n_params) - o;
+  prof_begin(c);
+  CKN(ncclAllReduce(c->grad + o, c->grad + o, (size_t)n, ncclFloat, ncclSum, c->comm, c->stream));
+  c->launches--;  // NCCL's kernel, not ours
+  return launch_check(c, HRP_K_ALLREDUCE);
+}
+
 // Backward over the first B rows on the tensor cores: operands are the transposed copies
-// (XT, actT, dzT) so every GEMM is K-major.  dz [B][H] -> c->grad.
-hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
+// (XT, actT, dhT) so every GEMM is K-major.  The head layer is the structured duelling-head
+// backward (k_head.cuh) from the per-sample descriptors td_kernel / tdq_kernel wrote.
+hrp_status mlp_backward(hrp_ctx* c, int B) {
   c->gemm_cls = HRP_K_GEMM_BWD;
   const int nl = (int)c->dims.size() - 1;
   const int H = c->dims[nl];
   const int Bp = c->Bp;
   const bool conc = concurrent(c);
   hrp_status s;
-  Pl dY = c->dz, dYT = c->dzT;
-  int ldy = c->ldz;
-  int top = nl - 1;
-  if (c->head_struct) {
+  Pl dY, dYT;
+  int ldy = 0;
+  int top;
+  {
     // head layer (nl - 1): dL/dh of the last hidden layer by gathers of W_head rows (main
     // stream), head weight / bias gradients by fp64 scatter-adds (side stream) -- k_head.cuh
     const int w = c->dims[nl - 1];
@@ -542,7 +534,8 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
       const int64_t n = (int64_t)H * (w + 1);
       prof_begin(c);
       head_finalize_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(h);
-      return launch_check(c, HRP_K_HEAD_BWD);
+      if ((t = launch_check(c, HRP_K_HEAD_BWD))) return t;
+      return allreduce_layer(c, nl - 1);
     };
     s = conc ? on_side(c, wgrad) : wgrad();
     if (s) return s;
@@ -555,11 +548,9 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
     dYT = c->dhTs[nl - 2];
     ldy = w;
     top = nl - 2;
-  } else {
-    if ((s = transpose(c, HRP_K_GEMM_BWD, B, H, c->ldz, c->dz, c->dzT, Bp))) return s;
-    if (conc && (s = fork(c))) return s;
   }
-  for (int i = top; i >= 0; --i) {    const int fi = c->dims[i], fo = c->dims[i + 1];
+  for (int i = top; i >= 0; --i) {
+    const int fi = c->dims[i], fo = c->dims[i + 1];
     const Pl HinT = (i == 0) ? c->XT : c->actT[i - 1];
     float* gW = c->grad + c->woff[i];
     float* gb = gW + (int64_t)fi * fo;
@@ -571,7 +562,8 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
                                    c->ws_splitk_elems, gW, gb);
       if (t) return fail(t, tc_gemm_error());
       c->launches += tc_gemm_launches(c->tc) - 1;
-      return launch_check(c, HRP_K_GEMM_BWD);
+      if ((t = launch_check(c, HRP_K_GEMM_BWD))) return t;
+      return allreduce_layer(c, i);
     };
     s = conc ? on_side(c, wgrad) : wgrad();
     if (s) return s;
@@ -591,42 +583,9 @@ hrp_status mlp_backward_tc(hrp_ctx* c, int B) {
   return HRP_OK;
 }
 
-// Backward over the first B rows (X rows [0,B), act rows [0,B)), dz [B][H] -> c->grad.
-// SIMT path: raw buffers.
-hrp_status mlp_backward(hrp_ctx* c, int B) {
-  if (tc_mode(c)) return mlp_backward_tc(c, B);
-  c->gemm_cls = HRP_K_GEMM_BWD;
-  const int nl = (int)c->dims.size() - 1;
-  const float* dY = c->dz.hi;
-  float* bufs[2] = {c->dh0, c->dh1};
-  int cur = 0;
-  for (int i = nl - 1; i >= 0; --i) {
-    const int fi = c->dims[i], fo = c->dims[i + 1];
-    const float* Hin = (i == 0) ? c->X.hi : c->act[i - 1].hi;
-    const int ldin = (i == 0) ? c->ldX : fi;
-    float* gW = c->grad + c->woff[i];
-    float* gb = gW + (int64_t)fi * fo;
-    // dW = dY^T . Hin  ([fo][fi]); reduction over the batch
-    hrp_status s = sgemm<false, false, EPI_STORE>(c, fo, fi, B, dY, fo, Hin, ldin, gW, fi,
-                                                  nullptr, nullptr, 0);
-    if (s) return s;
-    prof_begin(c);
-    colsum_kernel<<<(fo + 31) / 32, 256, 0, c->stream>>>(B, fo, dY, gb);
-    if ((s = launch_check(c, HRP_K_GEMM_BWD))) return s;
-    if (i > 0) {
-      const float* Wm = c->theta + c->woff[i];
-      float* dH = bufs[cur];
-      s = sgemm<true, false, EPI_RELU_MASK>(c, B, fi, fo, dY, fo, Wm, fi, dH, fi, nullptr, Hin, fi);
-      if (s) return s;
-      dY = dH;
-      cur ^= 1;
-    }
-  }
-  return HRP_OK;
-}
-
 hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.explicit_mode = c->explicit_mode;
+  a.err = c->dev_err;
   a.n_evals = c->n_evals;
   a.ctr = c->sched_ctr;
   prof_begin(c);
@@ -719,20 +678,7 @@ hrp_status hrp_nccl_unique_id(void* out) {
 }
 
 hrp_status hrp_env_destroy(hrp_ctx* c) {
-  if (!c) return HRP_OK;
-  cudaSetDevice(c->device);
-  cudaStreamSynchronize(c->stream);
-  if (c->comm) ncclCommDestroy(c->comm);
-  if (c->tc) tc_gemm_destroy(c->tc);
-  for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->side) {
-    cudaStreamSynchronize(c->side);
-    cudaStreamDestroy(c->side);
-  }
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
-  c->ar.release();
-  delete c;
+  delete c;   // ~hrp_ctx releases streams, events, NCCL comm, GEMM plans and device memory
   return HRP_OK;
 }
 
@@ -747,8 +693,9 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   if (s) return s;
   if (world < 1 || rank < 0 || rank >= world) return fail(HRP_EINVAL, "bad rank/world");
   if (world > 1 && !nccl_unique_id) return fail(HRP_EINVAL, "nccl_unique_id required for world > 1");
-  if (cfg->n_envs < 1 || cfg->batch < 1 || cfg->replay_capacity < cfg->batch)
-    return fail(HRP_ERANGE, "need n_envs >= 1, batch >= 1, replay_capacity >= batch");
+  if (cfg->n_envs < 1 || cfg->batch < 1 || cfg->replay_capacity < cfg->batch ||
+      cfg->replay_capacity < cfg->n_envs)
+    return fail(HRP_ERANGE, "need n_envs >= 1, batch >= 1, replay_capacity >= max(batch, n_envs)");
   if (cfg->n_envs > (1 << 24) || cfg->batch > (1 << 24) || cfg->replay_capacity > (1 << 28))
     return fail(HRP_ERANGE, "n_envs / batch / replay_capacity too large");
   if (cfg->hidden_layers < 1 || cfg->hidden_layers > 8 || cfg->hidden_width < 4 ||
@@ -778,8 +725,9 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   // argmax mode: explicit enumeration of every action needs the group tables (W <= 16)
   if (cfg->argmax_mode == 1 && hs.W > kXMaxW) return fail(HRP_ERANGE, "explicit argmax needs W <= 16");
   if (cfg->argmax_mode == 1 && hs.T > kXS) return fail(HRP_ERANGE, "explicit argmax needs <= 128 slot types");
-  c->explicit_mode = cfg->argmax_mode == 1 || (cfg->argmax_mode == 0 && hs.W <= kXMaxW && hs.T <= kXS);
-  c->gemm_mode = cfg->gemm_mode == 0 ? 2 : cfg->gemm_mode;
+  // auto = the exact pruned search (same actions bit for bit, faster at every measured config:
+  // cfg 2 0.394 vs 0.424 ms/step, profiles/r1zo_bench_cfg2*.json)
+  c->explicit_mode = cfg->argmax_mode == 1;
   if ((s = upload_tables(hs, prof, false, c->ar, c->stream, c->dt))) return s;
   // network dims and flat parameter layout (W [out][in] then b [out] per layer)
   c->dims.push_back(hs.W * kRowIn);
@@ -830,27 +778,21 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->rep_act, N * 8));
   CK(ar.alloc((void**)&c->rep_r, N * 4));
   CK(ar.alloc((void**)&c->rep_done, N));
-  const bool split = c->gemm_mode == 2;   // tensor-core path: operands stored as hi/lo planes
   c->Bp = r4(B);
-  c->ldX = split ? r4(in) : in;
-  c->ldz = split ? r4(H) : H;
+  c->ldX = r4(in);
   const size_t Bp = c->Bp;
   auto alloc_pl = [&](Pl& p, size_t n, bool two) -> cudaError_t {
     cudaError_t e = ar.alloc((void**)&p.hi, sizeof(float) * n);
     if (e == cudaSuccess && two) e = ar.alloc((void**)&p.lo, sizeof(float) * n);
     return e;
   };
-  CK(alloc_pl(c->X, R * c->ldX, split));
+  CK(alloc_pl(c->X, R * c->ldX, true));
   c->act.resize(cfg->hidden_layers);
-  for (auto& p : c->act) CK(alloc_pl(p, R * wd, split));
+  for (auto& p : c->act) CK(alloc_pl(p, R * wd, true));
   CK(ar.alloc((void**)&c->z, sizeof(float) * R * H));
-  CK(ar.alloc((void**)&c->zt, sizeof(float) * (size_t)B * H));
-  CK(alloc_pl(c->dz, (size_t)B * c->ldz, split));
-  CK(ar.alloc((void**)&c->dh0, sizeof(float) * (size_t)B * wd));
-  CK(ar.alloc((void**)&c->dh1, sizeof(float) * (size_t)B * wd));
   c->act_t.resize(cfg->hidden_layers);
-  for (auto& p : c->act_t) CK(alloc_pl(p, (size_t)B * wd, split));
-  if (split) {
+  for (auto& p : c->act_t) CK(alloc_pl(p, (size_t)B * wd, true));
+  {
     // transposed operands: zero padding columns [B, Bp) are never written.  X^T and the hidden
     // outputs^T carry one extra row of ones (hi 1, lo 0): the weight-gradient GEMM's product
     // with it is the bias gradient.
@@ -861,10 +803,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
       return e;
     };
     CK(alloc_pl(c->XT, Bp * (in + 1), true));
-    CK(alloc_pl(c->dzT, Bp * H, true));
     CK(ones_row(c->XT, in));
-    CK(cudaMemsetAsync(c->dzT.hi, 0, sizeof(float) * Bp * H, c->stream));
-    CK(cudaMemsetAsync(c->dzT.lo, 0, sizeof(float) * Bp * H, c->stream));
     c->actT.resize(cfg->hidden_layers);
     c->dhs.resize(cfg->hidden_layers);
     c->dhTs.resize(cfg->hidden_layers);
@@ -877,8 +816,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
         CK(cudaMemsetAsync(q, 0, sizeof(float) * Bp * wd, c->stream));
     }
   }
-  if (split) {
-    c->head_struct = true;
+  {
     const int T = hs.T;
     CK(ar.alloc((void**)&c->hdesc, sizeof(int) * 8 * (size_t)B));
     CK(ar.alloc((void**)&c->tdesc, sizeof(int) * 8 * (size_t)B));
@@ -898,11 +836,12 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->br, R * 4));
   CK(ar.alloc((void**)&c->bdone, R));
   CK(ar.alloc((void**)&c->dsq, R * 4));
-  CK(ar.alloc((void**)&c->tmp_i64, R * 8));
   CK(ar.alloc((void**)&c->n_evals, 16));  // [0] select / inference kernels, [1] TD kernel
   CK(cudaMemsetAsync(c->n_evals, 0, 16, c->stream));
   CK(ar.alloc((void**)&c->sched_ctr, 4 * sizeof(unsigned)));   // select, TD, tdq ticket
   CK(cudaMemsetAsync(c->sched_ctr, 0, 4 * sizeof(unsigned), c->stream));
+  CK(ar.alloc((void**)&c->dev_err, sizeof(unsigned)));
+  CK(cudaMemsetAsync(c->dev_err, 0, sizeof(unsigned), c->stream));
   if (init_weights) {
     CK(cudaMemcpyAsync(c->theta, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->theta_t, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
@@ -938,15 +877,12 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     CK(e);
   }
   c->p_grid = nsm * std::max(1, occ);
-  if (c->gemm_mode == 2) {
-    if ((s = tc_gemm_create(&c->tc, device, (int)R, c->dims.data(), (int)c->dims.size()))) {
-      return fail(s, tc_gemm_error());
-    }
-    CK(ar.alloc((void**)&c->wsplit, sizeof(float) * 4 * c->sstride));
-    CK(ar.alloc((void**)&c->wsplitT, sizeof(float) * 2 * c->sstride));
-    if ((s = split_weights(c.get(), false))) return s;
-    if ((s = split_weights(c.get(), true))) return s;
-  }
+  if ((s = tc_gemm_create(&c->tc, device, (int)R, c->dims.data(), (int)c->dims.size())))
+    return fail(s, tc_gemm_error());
+  CK(ar.alloc((void**)&c->wsplit, sizeof(float) * 4 * c->sstride));
+  CK(ar.alloc((void**)&c->wsplitT, sizeof(float) * 2 * c->sstride));
+  if ((s = split_weights(c.get(), false))) return s;
+  if ((s = split_weights(c.get(), true))) return s;
   if (world > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
@@ -1040,12 +976,16 @@ hrp_status hrp_q_forward(hrp_ctx* c, int64_t n, const uint8_t* d_windows, const 
   return HRP_OK;
 }
 
-hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_target, float* d_loss,
-                          int64_t* d_sample_idx, int64_t* d_astar) {
-  if (!c || !d_u_replay || !d_loss) return fail(HRP_EINVAL, "NULL argument");
+}  // extern "C"
+
+namespace {
+
+// a8-a12 of one double-DQN update: replay sample, forwards, TD argmax / loss, backward into
+// c->grad (allreduced per layer bucket when c->allreduce and world > 1).
+hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64_t* d_sample_idx,
+                    int64_t* d_astar) {
   const int B = c->cfg.batch;
   if (c->inserted < B) return fail(HRP_ESTATE, "replay holds fewer than batch transitions");
-  CK(cudaSetDevice(c->device));
   const int64_t nf = std::min<int64_t>(c->cfg.replay_capacity, c->inserted);
   const int H = c->hs.head_width();
   hrp_status s;
@@ -1057,9 +997,7 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
       c->rep_done, c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx, c->X.hi, c->X.lo,
       c->ldX);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
-  const bool tcb = tc_mode(c);
-  if (tcb && (s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->ldX, c->X, c->XT, c->Bp)))
-    return s;
+  if ((s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->ldX, c->X, c->XT, c->Bp))) return s;
   // online net on [s; s'] (activations of the s rows kept for backward) on the main stream,
   // target net on s' beside it (its own activation scratch)
   const bool conc = concurrent(c);
@@ -1077,18 +1015,16 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
     return launch_check(c, HRP_K_HEAD_BWD);
   };
   auto target_pass = [&]() -> hrp_status {
-    hrp_status t = mlp_forward(c, c->theta_t, c->X.off((size_t)B * c->ldX), B, c->zt, 0, &c->act_t,
-                               c->head_struct ? B : 0);
-    if (t || !c->head_struct) return t;
+    hrp_status t = mlp_forward(c, c->theta_t, c->X.off((size_t)B * c->ldX), B, nullptr, 0,
+                               &c->act_t, B);
+    if (t) return t;
     if ((t = head_means(c->theta_t, c->hc0t, c->hmTt))) return t;
     return head_means(c->theta, c->hc0, c->hmT);
   };
   if (conc) {
     if ((s = on_side(c, target_pass))) return s;
   }
-  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, tcb ? B : 0, nullptr,
-                       c->head_struct ? B : 0)))
-    return s;
+  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, B, nullptr, B))) return s;
   if (conc) {
     if ((s = join(c))) return s;
   } else if ((s = target_pass())) {
@@ -1097,7 +1033,6 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   TdArgs t{};
   t.B = B;
   t.z_all = c->z;
-  t.z_tgt = c->zt;
   t.bsched = c->bsched;
   t.bact = c->bact;
   t.br = c->br;
@@ -1105,11 +1040,9 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
   t.gamma = c->cfg.gamma;
   t.inv_btot = 1.f / ((float)B * (float)c->world);
   t.explicit_mode = c->explicit_mode;
-  t.dz = c->head_struct ? nullptr : c->dz.hi;
-  t.dz_lo = c->head_struct ? nullptr : c->dz.lo;
   t.hdesc = c->hdesc;
   t.tdesc = c->tdesc;
-  if (c->head_struct) {
+  {
     t.hs_hi = c->act[nl - 2].hi;
     t.hs_lo = c->act[nl - 2].lo;
     t.ht_hi = c->act_t[nl - 2].hi;
@@ -1121,11 +1054,11 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
     t.c0o = c->hc0; t.mTo = c->hmT; t.c0t = c->hc0t; t.mTt = c->hmTt;
     t.w = hw;
   }
-  t.ldz = c->ldz;
   t.dsq = c->dsq;
   t.astar = d_astar;
   t.n_evals = c->n_evals + 1;
   t.ctr = c->sched_ctr + 1;
+  t.err = c->dev_err;
   prof_begin(c);
   {
     const int rpc = sel_rows_per_cta(c->explicit_mode);
@@ -1135,67 +1068,86 @@ hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_targe
 #undef HRP_TD
   }
   if ((s = launch_check(c, HRP_K_TD))) return s;
-  if (c->head_struct) {
-    t.loss = d_loss;
-    t.done_ctr = c->sched_ctr + 2;
-    prof_begin(c);
-    tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(t);
-    if ((s = launch_check(c, HRP_K_TD))) return s;
-  } else {
-    prof_begin(c);
-    loss_kernel<<<1, 256, 0, c->stream>>>(B, c->dsq, d_loss);
-    if ((s = launch_check(c, HRP_K_MISC))) return s;
-  }
-  if ((s = mlp_backward(c, B))) return s;
-  if (c->world > 1) {
-    prof_begin(c);
-    CKN(ncclAllReduce(c->grad, c->grad, (size_t)c->n_params, ncclFloat, ncclSum, c->comm, c->stream));
-    c->launches--;  // NCCL's kernel, not ours
-    if ((s = launch_check(c, HRP_K_ALLREDUCE))) return s;
-  }
+  t.loss = d_loss;
+  t.done_ctr = c->sched_ctr + 2;
   prof_begin(c);
-  if (tc_mode(c)) {
-    SgdSplitArgs g{};
-    g.nl = (int)c->dims.size() - 1;
-    g.nlT = c->head_struct ? g.nl - 1 : g.nl;
-    g.n = c->n_params;
-    g.lr = c->cfg.lr;
-    g.th = c->theta;
-    g.g = c->grad;
-    g.tgt = c->theta_t;
-    g.sync = sync_target;
-    g.hi = c->wsplit;
-    g.lo = c->wsplit + c->sstride;
-    g.thi = c->wsplit + 2 * c->sstride;
-    g.tlo = c->wsplit + 3 * c->sstride;
-    g.hiT = c->wsplitT;
-    g.loT = c->wsplitT + c->sstride;
-    for (int i = 0; i < g.nl; ++i) {
-      g.woff[i] = c->woff[i];
-      g.soff[i] = c->soff[i];
-      g.soffT[i] = c->soffT[i];
-      g.fi[i] = c->dims[i];
-      g.fo[i] = c->dims[i + 1];
-    }
-    g.woff[g.nl] = c->n_params;
-    sgd_split_kernel<<<8 * 148, 256, 0, c->stream>>>(g);
-  } else {
-    sgd_kernel<<<4 * 148, 256, 0, c->stream>>>(c->n_params, c->cfg.lr, c->theta, c->grad,
-                                                c->theta_t, sync_target);
+  tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(t);
+  if ((s = launch_check(c, HRP_K_TD))) return s;
+  return mlp_backward(c, B);
+}
+
+// a13: SGD from the gradient g (c->grad, or an imported one), target sync, tf32 re-split.
+hrp_status apply_grad(hrp_ctx* c, const float* grad, int sync_target) {
+  prof_begin(c);
+  SgdSplitArgs g{};
+  g.nl = (int)c->dims.size() - 1;
+  g.nlT = g.nl - 1;
+  g.n = c->n_params;
+  g.lr = c->cfg.lr;
+  g.th = c->theta;
+  g.g = grad;
+  g.tgt = c->theta_t;
+  g.sync = sync_target;
+  g.hi = c->wsplit;
+  g.lo = c->wsplit + c->sstride;
+  g.thi = c->wsplit + 2 * c->sstride;
+  g.tlo = c->wsplit + 3 * c->sstride;
+  g.hiT = c->wsplitT;
+  g.loT = c->wsplitT + c->sstride;
+  for (int i = 0; i < g.nl; ++i) {
+    g.woff[i] = c->woff[i];
+    g.soff[i] = c->soff[i];
+    g.soffT[i] = c->soffT[i];
+    g.fi[i] = c->dims[i];
+    g.fo[i] = c->dims[i + 1];
   }
-  if ((s = launch_check(c, HRP_K_SGD))) return s;
-  (void)H;
+  g.woff[g.nl] = c->n_params;
+  sgd_split_kernel<<<8 * 148, 256, 0, c->stream>>>(g);
+  return launch_check(c, HRP_K_SGD);
+}
+
+}  // namespace
+
+extern "C" {
+
+hrp_status hrp_dqn_update(hrp_ctx* c, const uint32_t* d_u_replay, int sync_target, float* d_loss,
+                          int64_t* d_sample_idx, int64_t* d_astar) {
+  if (!c || !d_u_replay || !d_loss) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  c->allreduce = true;
+  hrp_status s = dqn_grad(c, d_u_replay, d_loss, d_sample_idx, d_astar);
+  if (s) return s;
+  return apply_grad(c, c->grad, sync_target);
+}
+
+hrp_status hrp_dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss,
+                        int64_t* d_sample_idx, int64_t* d_astar, float* d_grad) {
+  if (!c || !d_u_replay || !d_loss || !d_grad) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  c->allreduce = false;
+  hrp_status s = dqn_grad(c, d_u_replay, d_loss, d_sample_idx, d_astar);
+  c->allreduce = true;
+  if (s) return s;
+  CK(cudaMemcpyAsync(d_grad, c->grad, sizeof(float) * c->n_params, cudaMemcpyDeviceToDevice,
+                     c->stream));
   return HRP_OK;
 }
 
-hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* prof, int64_t n,
-                                  const uint8_t* d_windows, int64_t* d_best, int64_t* d_solo,
-                                  uint8_t* d_rgs, int64_t* d_bact, void* cuda_stream) {
-  if (!d_windows || !d_best || !d_solo || !d_rgs || !d_bact) return fail(HRP_EINVAL, "NULL argument");
-  if (n < 0) return fail(HRP_EINVAL, "n < 0");
+hrp_status hrp_apply_grad(hrp_ctx* c, const float* d_grad, int sync_target) {
+  if (!c || !d_grad) return fail(HRP_EINVAL, "NULL argument");
+  CK(cudaSetDevice(c->device));
+  return apply_grad(c, d_grad, sync_target);
+}
+
+
+hrp_status hrp_brute_create(const hrp_space* space, const hrp_profiles* prof, int device,
+                            void* cuda_stream, hrp_brute** out) {
+  if (!out) return fail(HRP_EINVAL, "out is NULL");
+  *out = nullptr;
   hrp_status s = validate_pool(prof);
   if (s) return s;
-  HostSpace hs;
+  std::unique_ptr<hrp_brute> b(new hrp_brute());
+  HostSpace& hs = b->hs;
   try {
     std::string err;
     if ((s = build_space(space, hs, err))) return fail(s, err);
@@ -1210,12 +1162,12 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
   int nb8 = 0, b8v[kBruteMaxB8] = {0, 0, 0, 0};
   for (int l = 0; l < hs.L; ++l)
     for (int k = 0; k < hs.nslots[l]; ++k) {
-      const int b = hs.slots[l][k].b8;
+      const int v = hs.slots[l][k].b8;
       bool seen = false;
-      for (int q = 0; q < nb8; ++q) seen |= b8v[q] == b;
+      for (int q = 0; q < nb8; ++q) seen |= b8v[q] == v;
       if (!seen) {
         if (nb8 == kBruteMaxB8) return fail(HRP_ERANGE, "brute force: more than 4 memory sizes");
-        b8v[nb8++] = b;
+        b8v[nb8++] = v;
       }
     }
   int n_items = 0;
@@ -1234,35 +1186,62 @@ hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* pr
                                   (double)tmax * 4000.0 / (5.0 * std::max(1, min_sm)) + 1.0);
     if (bound >= 4294967296.0) return fail(HRP_ERANGE, "brute force: solo ticks too large");
   }
+  b->device = device;
+  CK(cudaSetDevice(device));
+  if ((s = init_constants(device))) return s;
+  if ((s = upload_tables(hs, prof, true, b->ar, (cudaStream_t)cuda_stream, b->dt))) return s;
+  b->smem = brute_smem_bytes(hs.W, hs.T, n_items);
+  if (b->smem > 227 * 1024) return fail(HRP_ERANGE, "brute force: layout space too large for shared memory");
+  static int brute_smem_max[64] = {0};
+  if ((int)b->smem > brute_smem_max[device & 63]) {
+    CK(cudaFuncSetAttribute(brute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->smem));
+    brute_smem_max[device & 63] = (int)b->smem;
+  }
+  int nsm = 148, occ = 1;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brute_kernel, kBruteThreads, b->smem));
+  b->grid_max = nsm * std::max(1, occ);
+  b->nb8 = nb8;
+  for (int q = 0; q < kBruteMaxB8; ++q) b->b8v[q] = b8v[q];
+  b->n_items = n_items;
+  *out = b.release();
+  return HRP_OK;
+}
+
+hrp_status hrp_brute_run(hrp_brute* b, int64_t n, const uint8_t* d_windows, int64_t* d_best,
+                         int64_t* d_solo, uint8_t* d_rgs, int64_t* d_bact, void* cuda_stream) {
+  if (!b || !d_windows || !d_best || !d_solo || !d_rgs || !d_bact) return fail(HRP_EINVAL, "NULL argument");
+  if (n < 0 || n > INT32_MAX) return fail(HRP_ERANGE, "n outside 0..2^31-1");
   if (n == 0) return HRP_OK;
+  CK(cudaSetDevice(b->device));
+  const int grid = (int)std::min<int64_t>(n, b->grid_max);
+  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact, b->nb8,
+              {b->b8v[0], b->b8v[1], b->b8v[2], b->b8v[3]}, b->n_items};
+  brute_kernel<<<grid, kBruteThreads, b->smem, (cudaStream_t)cuda_stream>>>(b->dt.sp, b->dt.pool, a);
+  CK(cudaGetLastError());
+  return HRP_OK;
+}
+
+hrp_status hrp_brute_destroy(hrp_brute* b) {
+  delete b;
+  return HRP_OK;
+}
+
+hrp_status hrp_bruteforce_optimum(const hrp_space* space, const hrp_profiles* prof, int64_t n,
+                                  const uint8_t* d_windows, int64_t* d_best, int64_t* d_solo,
+                                  uint8_t* d_rgs, int64_t* d_bact, void* cuda_stream) {
+  if (!d_windows || !d_best || !d_solo || !d_rgs || !d_bact) return fail(HRP_EINVAL, "NULL argument");
+  if (n < 0) return fail(HRP_EINVAL, "n < 0");
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  if ((s = init_constants(dev))) return s;
-  cudaStream_t st = (cudaStream_t)cuda_stream;
-  Arena ar;
-  DevTables dt;
-  if ((s = upload_tables(hs, prof, true, ar, st, dt))) { ar.release(); return s; }
-  const size_t smem = brute_smem_bytes(hs.W, hs.T, n_items);
-  if (smem > 227 * 1024) { ar.release(); return fail(HRP_ERANGE, "brute force: layout space too large for shared memory"); }
-  static int brute_smem_max[64] = {0};
-  cudaError_t e = cudaSuccess;
-  if ((int)smem > brute_smem_max[dev & 63]) {
-    e = cudaFuncSetAttribute(brute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) brute_smem_max[dev & 63] = (int)smem;
-  }
-  if (e != cudaSuccess) { ar.release(); return fail(HRP_ECUDA, cudaGetErrorString(e)); }
-  int nsm = 148, occ = 1;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, brute_kernel, kBruteThreads, smem);
-  const int grid = (int)std::min<int64_t>(n, (int64_t)nsm * std::max(1, occ));
-  BruteArgs a{(int)n, d_windows, d_best, d_solo, d_rgs, d_bact, nb8, {b8v[0], b8v[1], b8v[2], b8v[3]},
-               n_items};
-  brute_kernel<<<grid, kBruteThreads, smem, st>>>(dt.sp, dt.pool, a);
-  e = cudaGetLastError();
-  cudaError_t e2 = cudaStreamSynchronize(st);
-  ar.release();
+  hrp_brute* b = nullptr;
+  hrp_status s = hrp_brute_create(space, prof, dev, cuda_stream, &b);
+  if (s) return s;
+  s = hrp_brute_run(b, n, d_windows, d_best, d_solo, d_rgs, d_bact, cuda_stream);
+  const cudaError_t e = cudaStreamSynchronize((cudaStream_t)cuda_stream);
+  hrp_brute_destroy(b);
+  if (s) return s;
   if (e != cudaSuccess) return fail(HRP_ECUDA, cudaGetErrorString(e));
-  if (e2 != cudaSuccess) return fail(HRP_ECUDA, cudaGetErrorString(e2));
   return HRP_OK;
 }
 
@@ -1381,6 +1360,13 @@ hrp_status hrp_sync(hrp_ctx* c) {
   if (!c) return fail(HRP_EINVAL, "NULL argument");
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
+  unsigned err = 0;
+  CK(cudaMemcpy(&err, c->dev_err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err) {
+    CK(cudaMemset(c->dev_err, 0, sizeof(err)));
+    return fail(HRP_ENUMERIC, "non-finite Q values: a greedy argmax found no comparable action "
+                              "(the lowest valid action was taken instead)");
+  }
   if (c->comm) {
     ncclResult_t r;
     CKN(ncclCommGetAsyncError(c->comm, &r));

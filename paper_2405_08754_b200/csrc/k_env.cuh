@@ -3,7 +3,7 @@
 //   sample_encode_kernel  a8 + a2 replay sampling fused with the encoding of s and s'
 // plus the device helpers of the selection / TD kernels (k_select.cuh): co-run time (a6),
 // valid-action count, permutation order, and their argument blocks.
-//   sgd_kernel         a13 SGD + target sync
+//   sgd_split_kernel   a13 SGD + target sync + tf32 re-split
 #pragma once
 #include "dev.cuh"
 
@@ -191,6 +191,7 @@ struct SelArgs {
   int N_rep;
   unsigned long long* n_evals;  // optional evaluation counter
   unsigned* ctr;                // dynamic row scheduler (self-resetting, zero at create)
+  unsigned* err;                // device error flag (bit 0: non-finite Q, see hrp_sync)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -241,8 +242,7 @@ __global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uin
 
 struct TdArgs {
   int B;
-  const float* z_all;   // [2B][H]: rows [0,B) online(s), [B,2B) online(s')
-  const float* z_tgt;   // [B][H] target(s')
+  const float* z_all;   // [2B][H]: rows [B,2B) online(s') (rows [0,B) are not computed)
   const uint64_t* bsched;  // [2B]
   const int64_t* bact;
   const float* br;
@@ -250,16 +250,13 @@ struct TdArgs {
   float gamma;
   float inv_btot;       // 1 / (B * world)
   bool explicit_mode;
-  float* dz;            // [B][H] raw, or the hi plane when dz_lo != NULL
-  float* dz_lo;         // [B][H] lo plane (tensor-core path) or NULL
-  int ldz;              // row stride of dz
   float* dsq;           // [B]
-  int* tdesc;           // structured mode: [B][8] descriptor of a* (word 2 = -1 when done)
-  int* hdesc;           // structured head gradient (dz == NULL): [B][8] per sample
+  int* tdesc;           // [B][8] descriptor of a* (word 2 = -1 when done)
+  int* hdesc;           // structured head gradient: [B][8] per sample
                         //   {sc bits, 1 + l, C, rows 1 + L + g_i T + t_i (i < C; -1 pad) x 4,
                         //    t_0 | t_1 << 8 | t_2 << 16 | t_3 << 24}, sc = delta / (B world)
   int64_t* astar;       // [B] optional
-  // sparse Q (hdesc mode): Q(s, a) and Q_target(s', a*) from the last hidden activations and the
+  // sparse Q: Q(s, a) and Q_target(s', a*) from the last hidden activations and the
   // head rows they need, Q = h . (c0 + W[1 + l] + sum_i (W[r_i] - mT[t_i])) + (same on biases),
   // instead of full online-head rows for s and target-head rows for s'
   const float* hs_hi;   // online last hidden activation of the s rows [B][w], hi / lo planes
@@ -275,24 +272,14 @@ struct TdArgs {
   const float* c0t;
   const float* mTt;
   int w;
-  float* loss;          // structured mode: tdq_kernel's last block writes the loss here
+  float* loss;          // tdq_kernel's last block writes the loss here
   unsigned* done_ctr;   //   block ticket counter (zero between launches)
   unsigned long long* n_evals;
   unsigned* ctr;        // dynamic row scheduler (self-resetting, zero at create)
+  unsigned* err;        // device error flag (bit 0: non-finite Q, see hrp_sync)
 };
 
-// a13: theta -= lr * g ; optional target sync.
-__global__ void sgd_kernel(int64_t n, float lr, float* __restrict__ th, const float* __restrict__ g,
-                           float* __restrict__ tgt, int sync) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = th[i] - lr * g[i];
-    th[i] = v;
-    if (sync) tgt[i] = v;
-  }
-}
-
-// a13 on the tensor-core path, one launch: theta -= lr * g, the 3xTF32 hi / lo planes of every
+// a13, one launch: theta -= lr * g, the 3xTF32 hi / lo planes of every
 // weight matrix re-split from the new value (W [fo][ldw] and W^T [fi][ldt] planes), and on a
 // target-sync step the target parameters and their planes too (identical values).
 constexpr int kMaxLayers = 9;
@@ -339,15 +326,6 @@ __global__ void sgd_split_kernel(SgdSplitArgs a) {
     a.hiT[ot] = h;
     a.loT[ot] = lw;
   }
-}
-
-// loss = sum dsq / (2B), single block, deterministic.
-__global__ void loss_kernel(int B, const float* __restrict__ dsq, float* __restrict__ loss) {
-  __shared__ float red[32];
-  float acc = 0.f;
-  for (int i = threadIdx.x; i < B; i += blockDim.x) acc += dsq[i];
-  acc = block_sum(acc, red);
-  if (threadIdx.x == 0) *loss = acc / (2.f * (float)B);
 }
 
 }  // namespace hrp

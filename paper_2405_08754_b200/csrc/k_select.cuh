@@ -718,6 +718,12 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
       const int64_t nv = n_valid(sp, sched);
       const int64_t k = (int64_t)__umul64hi(a.u_action[row], (uint64_t)nv);
       act = pwarp_kth_valid(sp, tb, sched, k);
+    } else if (bidx == INT64_MAX) {
+      // a state always has a valid action, so no maximiser means non-finite Q values (NaN
+      // weights): flag it for hrp_sync and keep the environment consistent with the lowest
+      // valid action
+      if (lane == 0) atomicOr(a.err, 1u);
+      act = pwarp_kth_valid(sp, tb, sched, 0);
     }
     const uint8_t* wr = a.win + (size_t)row * W;
     int64_t slot = 0;
@@ -765,7 +771,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
       a.done[row] = (uint8_t)d;
       if (a.corun) a.corun[row] = cr;
       if (a.qsel) a.qsel[row] = (float)((double)q * (1.0 / 4294967296.0));
-      if (a.greedy) a.greedy[row] = bidx;
+      if (a.greedy) a.greedy[row] = bidx == INT64_MAX ? -1 : bidx;
       a.sched[row] = d ? 0ull : s2;
     }
     slot = __shfl_sync(0xffffffffu, slot, 0);
@@ -782,26 +788,6 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     if (lane == 0 && tot) atomicAdd(a.n_evals, (unsigned long long)tot);
   }
-}
-
-// Float Q(s, a) of action idx from a global head row, warp-cooperative means.
-__device__ inline float pwarp_qfloat(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
-                                     const float* __restrict__ z, int64_t idx, int* l_out,
-                                     int* g_out, int* t_out) {
-  const float meanL = pwarp_means(sp, z, w.meanJ);
-  int g[4], sg[4];
-  const int l = decode_action(sp, idx, g, sg);
-  const uint32_t ty = tb.stype[l];
-  const int C = tb.nsl[l];
-  float q = z[0] + (z[1 + l] - meanL);
-  for (int i = 0; i < C; ++i) {
-    const int t = (ty >> (8 * sg[i])) & 255;
-    q += z[1 + sp.L + g[i] * sp.T + t] - w.meanJ[t];
-    if (g_out) { g_out[i] = g[i]; t_out[i] = t; }
-  }
-  if (l_out) *l_out = l;
-  __syncwarp();
-  return q;
 }
 
 // Action idx -> layout, members g_i and their slot types t_i (returns l; C = nsl[l]).
@@ -913,77 +899,28 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * pwarps(X > 0);
-  const int H = sp.H, L = sp.L, T = sp.T, W = sp.W;
   int64_t nevals = 0;
   for (int b = next_row(a.ctr, a.B, nw); b < a.B; b = next_row(a.ctr, a.B, nw)) {
     const bool done = a.bdone[b] != 0;
-    float y = a.br[b];
     int64_t astar = -1;
-    if (a.dz == nullptr) {
-      // structured mode: the argmax a* on s' here; both Q values, delta and the loss terms in
-      // tdq_kernel from the action descriptors (tdesc: a*, hdesc: a)
-      if (!done) {
-        const float* zn = a.z_all + (size_t)(a.B + b) * H;
-        const float meanL = pwarp_means(sp, zn, w.meanJ);
-        int64_t best;
-        greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
-      }
-      if (lane == 0 && a.astar) a.astar[b] = astar;
-      write_desc(sp, tb, a.bact[b], a.hdesc + (size_t)b * 8);
-      if (done) {
-        if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
-      } else {
-        write_desc(sp, tb, astar, a.tdesc + (size_t)b * 8);
-      }
-      __syncwarp();
-      continue;
-    }
+    // the argmax a* on s' here; both Q values, delta and the loss terms in tdq_kernel from the
+    // action descriptors (tdesc: a*, hdesc: a)
     if (!done) {
-      const float* zg = a.z_all + (size_t)(a.B + b) * H;
-      const float* zn = zg;
+      const float* zn = a.z_all + (size_t)(a.B + b) * sp.H;
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
-      const float* tg = a.z_tgt + (size_t)b * H;
-      const float qt = pwarp_qfloat(sp, tb, w, tg, astar, nullptr, nullptr, nullptr);
-      y = a.br[b] + a.gamma * qt;
-    }
-    int l, g[4], tt[4];
-    const float* og = a.z_all + (size_t)b * H;
-    const float q = pwarp_qfloat(sp, tb, w, og, a.bact[b], &l, g, tt);
-    const int C = tb.nsl[l];
-    const float delta = q - y;
-    if (lane == 0) {
-      a.dsq[b] = delta * delta;
-      if (a.astar) a.astar[b] = astar;
-    }
-    const float sc = delta * a.inv_btot;
-    const float invL = 1.f / (float)L, invW = 1.f / (float)W;
-    float* dzr = a.dz + (size_t)b * a.ldz;
-    float* dzl = a.dz_lo ? a.dz_lo + (size_t)b * a.ldz : nullptr;
-    // dQ/dz: v -> 1; aL[l'] -> [l' = l] - 1/L; aJ[j][t] -> #{i: g_i = j, t_i = t} - #{i: t_i = t}/W
-    for (int h = lane; h < H; h += 32) {
-      float dv;
-      if (h == 0) dv = 1.f;
-      else if (h <= L) dv = (h - 1 == l ? 1.f : 0.f) - invL;
-      else {
-        const int qq = h - 1 - L;
-        const int j = qq / T, t = qq - j * T;
-        int cjt = 0, ct = 0;
-        for (int i = 0; i < C; ++i) {
-          ct += tt[i] == t;
-          cjt += (tt[i] == t) && (g[i] == j);
-        }
-        dv = (float)cjt - (float)ct * invW;
+      if (astar == INT64_MAX) {   // non-finite Q (see sel_kernel): flag, lowest valid action
+        if (lane == 0) atomicOr(a.err, 1u);
+        astar = pwarp_kth_valid(sp, tb, a.bsched[a.B + b], 0);
       }
-      const float g = dv * sc;
-      if (dzl) {
-        const float hh = tf32_rna(g);
-        dzr[h] = hh;
-        dzl[h] = g - hh;
-      } else {
-        dzr[h] = g;
-      }
+    }
+    if (lane == 0 && a.astar) a.astar[b] = astar;
+    write_desc(sp, tb, a.bact[b], a.hdesc + (size_t)b * 8);
+    if (done) {
+      if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
+    } else {
+      write_desc(sp, tb, astar, a.tdesc + (size_t)b * 8);
     }
     __syncwarp();
   }

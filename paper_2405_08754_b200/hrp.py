@@ -15,8 +15,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhrp.so")
 
-HRP_OK, HRP_EINVAL, HRP_ENOMEM, HRP_ECUDA, HRP_ENCCL, HRP_ERANGE, HRP_ESTATE = range(7)
-STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ERANGE", 6: "ESTATE"}
+HRP_OK, HRP_EINVAL, HRP_ENOMEM, HRP_ECUDA, HRP_ENCCL, HRP_ERANGE, HRP_ESTATE, HRP_ENUMERIC = \
+    range(8)
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ERANGE", 6: "ESTATE",
+          7: "ENUMERIC"}
 
 
 class HrpError(RuntimeError):
@@ -43,8 +45,7 @@ class hrp_space(C.Structure):
 class hrp_train_cfg(C.Structure):
     _fields_ = [("n_envs", C.c_int32), ("batch", C.c_int32), ("replay_capacity", C.c_int32),
                 ("hidden_layers", C.c_int32), ("hidden_width", C.c_int32), ("gamma", C.c_float),
-                ("lr", C.c_float), ("reward_lambda", C.c_float), ("argmax_mode", C.c_int32),
-                ("gemm_mode", C.c_int32)]
+                ("lr", C.c_float), ("reward_lambda", C.c_float), ("argmax_mode", C.c_int32)]
 
 
 _lib = None
@@ -65,7 +66,12 @@ def lib():
             "hrp_env_step": [P, u64, P, P, P, P, P, P, P, P, P],
             "hrp_q_forward": [P, i64, P, P, P, P, P],
             "hrp_dqn_update": [P, P, S, P, P, P],
+            "hrp_dqn_grad": [P, P, P, P, P, P],
+            "hrp_apply_grad": [P, P, S],
             "hrp_bruteforce_optimum": [P, P, i64, P, P, P, P, P, P],
+            "hrp_brute_create": [P, P, S, P, P],
+            "hrp_brute_run": [P, i64, P, P, P, P, P, P],
+            "hrp_brute_destroy": [P],
             "hrp_layout_table": [P, i32, P, P, P, P, P, P],
             "hrp_decode_action": [P, i64, P, P, P],
             "hrp_get_weights": [P, P],
@@ -136,9 +142,9 @@ def make_profiles(pool):
 
 
 def make_cfg(n_envs, batch, replay_capacity, hidden_layers, hidden_width, gamma=0.99, lr=1e-3,
-             reward_lambda=0.0, argmax_mode=0, gemm_mode=0):
+             reward_lambda=0.0, argmax_mode=0):
     return hrp_train_cfg(n_envs, batch, replay_capacity, hidden_layers, hidden_width, gamma, lr,
-                         reward_lambda, argmax_mode, gemm_mode)
+                         reward_lambda, argmax_mode)
 
 
 # ---- entry points (same names as the C ABI) ---------------------------------------------
@@ -183,6 +189,31 @@ def hrp_q_forward(ctx, n, d_windows, d_sched, d_argmax, d_qmax, d_head=None):
 def hrp_dqn_update(ctx, d_u_replay, sync_target, d_loss, d_sample_idx=None, d_astar=None):
     _check(lib().hrp_dqn_update(ctx, _ptr(d_u_replay), int(bool(sync_target)), _ptr(d_loss),
                                 _ptr(d_sample_idx), _ptr(d_astar)))
+
+
+def hrp_dqn_grad(ctx, d_u_replay, d_loss, d_grad, d_sample_idx=None, d_astar=None):
+    _check(lib().hrp_dqn_grad(ctx, _ptr(d_u_replay), _ptr(d_loss), _ptr(d_sample_idx),
+                              _ptr(d_astar), _ptr(d_grad)))
+
+
+def hrp_apply_grad(ctx, d_grad, sync_target):
+    _check(lib().hrp_apply_grad(ctx, _ptr(d_grad), int(bool(sync_target))))
+
+
+def hrp_brute_create(space, profiles, device, cuda_stream):
+    plan = C.c_void_p()
+    _check(lib().hrp_brute_create(C.byref(space), C.byref(profiles), device,
+                                  C.c_void_p(cuda_stream), C.byref(plan)))
+    return plan
+
+
+def hrp_brute_run(plan, n, d_windows, d_best, d_solo, d_rgs, d_bact, cuda_stream):
+    _check(lib().hrp_brute_run(plan, int(n), _ptr(d_windows), _ptr(d_best), _ptr(d_solo),
+                               _ptr(d_rgs), _ptr(d_bact), C.c_void_p(cuda_stream)))
+
+
+def hrp_brute_destroy(plan):
+    _check(lib().hrp_brute_destroy(plan))
 
 
 def hrp_bruteforce_optimum(space, profiles, n, d_windows, d_best, d_solo, d_rgs, d_bact,

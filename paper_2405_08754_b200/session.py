@@ -16,7 +16,7 @@ def space_of(scfg, layouts=None):
 
 class Session:
     def __init__(self, cfg, pool, n_envs=None, batch=None, init_weights=None, device=0,
-                 rank=0, world=1, nccl_id=None, argmax_mode=0, gemm_mode=0, replay=None,
+                 rank=0, world=1, nccl_id=None, argmax_mode=0, replay=None,
                  reward_lambda=None, stream=None):
         if not torch.cuda.is_available():
             raise RuntimeError("libhrp needs a CUDA device (no CPU fallback)")
@@ -31,7 +31,7 @@ class Session:
         lam = cfg.space.reward_lambda if reward_lambda is None else reward_lambda
         self.tcfg = hrp.make_cfg(self.E, self.B, replay or max(1 << 16, 16 * self.E),
                                  cfg.net.hidden_layers, cfg.net.hidden_width, cfg.gamma, cfg.lr,
-                                 lam, argmax_mode, gemm_mode)
+                                 lam, argmax_mode)
         self.ctx = hrp.hrp_env_create(self.space, self.prof, self.tcfg, device,
                                       self.stream.cuda_stream, rank, world, nccl_id,
                                       init_weights)
@@ -75,6 +75,14 @@ class Session:
     def update(self, u_replay, sync_target, extras=True):
         hrp.hrp_dqn_update(self.ctx, u_replay, sync_target, self.loss,
                            self.sidx if extras else None, self.astar if extras else None)
+
+    def grad(self, u_replay, d_grad, extras=True):
+        """hrp_dqn_grad: this rank's gradient into d_grad (no allreduce, weights unchanged)."""
+        hrp.hrp_dqn_grad(self.ctx, u_replay, self.loss, d_grad,
+                         self.sidx if extras else None, self.astar if extras else None)
+
+    def apply_grad(self, d_grad, sync_target):
+        hrp.hrp_apply_grad(self.ctx, d_grad, sync_target)
 
     def q_forward(self, windows, sched, head=False):
         n = windows.shape[0]

@@ -80,3 +80,34 @@ def test_restricted_baselines_table_v(name):
     pool = synth.make_pool(27)
     scfg, lay = synth.BASELINE_SPACES[name]
     _cmp(scfg, pool, synth.table_v_windows(pool), layouts=lay)
+
+
+def test_resident_plan_equals_one_shot_and_is_graph_capturable():
+    # hrp_brute_create / run / destroy: tables uploaded once, the run only enqueues the kernel
+    # (captured in a CUDA graph here); results equal the one-shot call and the oracle on Q1-Q12
+    import torch
+    from paper_2405_08754_b200 import hrp
+    from paper_2405_08754_b200.session import bruteforce, space_of
+    pool = synth.make_pool(27)
+    scfg = SpaceCfg(12, 4, S10)
+    wins = np.concatenate([synth.table_v_windows(pool), synth.make_windows(pool, 20, 12, step=7)])
+    n = len(wins)
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.Stream(dev)
+    plan = hrp.hrp_brute_create(space_of(scfg), hrp.make_profiles(pool), 0, st.cuda_stream)
+    with torch.cuda.stream(st):
+        w = torch.from_numpy(wins).to(dev)
+        outs = [torch.full((n,), -7, dtype=torch.int64, device=dev),
+                torch.full((n,), -7, dtype=torch.int64, device=dev),
+                torch.zeros((n, 12), dtype=torch.uint8, device=dev),
+                torch.zeros((n, 12), dtype=torch.int64, device=dev)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            hrp.hrp_brute_run(plan, n, w, *outs, st.cuda_stream)
+        g.replay()
+    st.synchronize()
+    hrp.hrp_brute_destroy(plan)
+    ref = bruteforce(scfg, pool, wins)
+    for a, b in zip(outs, ref):
+        np.testing.assert_array_equal(a.cpu().numpy(), b)
+    _cmp(scfg, pool, wins[:12])

@@ -1,5 +1,10 @@
 """GPU parity of the DQN step (hrp_env_step + hrp_dqn_update) and inference (hrp_q_forward)
-against the float64 oracle, in lockstep over seeded steps (tests/dqn_harness.py)."""
+against the float64 oracle, in lockstep over seeded steps (tests/dqn_harness.py).
+
+Sizes follow SURVEY §8(c) "Parity protocol": config 1 in full (E = B = 64, 100 steps);
+config 2 at E = B = 256 for 100 steps (the weight-gradient GEMM runs split-K with S >= 8, the
+reduce's 8-wide path) and in the bench's launch configuration E = B = 4096 for 3 steps;
+config 4 (W = 64, Cmax = 4, 4 x 512, P = 256, pruned argmax) at E = B = 64 for 20 steps."""
 import numpy as np
 import pytest
 import torch
@@ -9,21 +14,16 @@ from oracle import env as EV
 from oracle import pruned as PR
 from oracle import qnet as QN
 from oracle import space as SP
-from dqn_harness import close, make_pair, run_lockstep
+from dqn_harness import close, check_near_ties, log_stats, make_pair, run_lockstep
 
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("gemm_mode", [1, 2])
-def test_config1_100_steps(gemm_mode):
+@pytest.mark.parametrize("argmax_mode", [1, 2])
+def test_config1_100_steps(argmax_mode):
     # BASELINE config 1: W=4, Cmax=2, S={25,50,75}, MLP 2x64, 64 envs, 100 steps
-    st = run_lockstep(1, 64, 64, 100, gemm_mode=gemm_mode, argmax_mode=1,
-                      check_weights_every=1)
-    print(st)
-
-
-def test_config1_pruned_argmax():
-    st = run_lockstep(1, 64, 64, 30, argmax_mode=2)
+    st = run_lockstep(1, 64, 64, 100, argmax_mode=argmax_mode, check_weights_every=1,
+                      oracle_argmax="explicit")
     print(st)
 
 
@@ -39,11 +39,30 @@ def test_ragged_sizes():
     print(st)
 
 
-@pytest.mark.parametrize("gemm_mode", [1, 2])
-def test_config2_reduced(gemm_mode):
-    # BASELINE config 2 space + net (W=16, Cmax=3, S={10..90}, 3x256) at E=B=48
-    st = run_lockstep(2, 48, 48, 8, gemm_mode=gemm_mode, argmax_mode=1,
-                      check_weights_every=2)
+def test_config2_explicit_vs_explicit_oracle():
+    # config 2 space + net, explicit GPU enumeration against the oracle's explicit enumeration
+    st = run_lockstep(2, 48, 48, 8, argmax_mode=1, check_weights_every=2,
+                      oracle_argmax="explicit")
+    print(st)
+
+
+def test_config2_256_envs_100_steps():
+    # SURVEY protocol: config 2 at E = B = 256 for 100 seeded steps (split-K S >= 8 in every
+    # weight-gradient GEMM, target syncs at steps 25/50/75/100, weights checked every 10 steps)
+    st = run_lockstep(2, 256, 256, 100, check_weights_every=10)
+    print(st)
+
+
+def test_config2_full_size_3_steps():
+    # the bench's launch configuration: E = B = 4096, every output and the weights compared
+    # element by element after each of 3 steps
+    st = run_lockstep(2, 4096, 4096, 3)
+    print(st)
+
+
+def test_config4_64_envs_20_steps():
+    # config 4: W = 64, Cmax = 4, 4 x 512, H = 5379, pool of 256, pruned exact argmax
+    st = run_lockstep(4, 64, 64, 20, check_weights_every=5)
     print(st)
 
 
@@ -55,7 +74,7 @@ def _states(pool, n, W, seed):
 
 @pytest.mark.parametrize("cfgk,n,mode", [(1, 200, 1), (2, 96, 1), (2, 96, 2)])
 def test_q_forward_parity(cfgk, n, mode):
-    cfg, pool, osp, sess, orc = make_pair(cfgk, 64, 64, argmax_mode=mode)
+    cfg, pool, osp, sess, orc = make_pair(cfgk, 64, 64, argmax_mode=mode, workers=0)
     wins, sched = _states(pool, n, osp.W, 5)
     dw = torch.from_numpy(wins).to(sess.dev)
     ds = torch.from_numpy(sched.view(np.int64)).to(sess.dev)
@@ -65,7 +84,9 @@ def test_q_forward_parity(cfgk, n, mode):
     np.testing.assert_array_equal(am.cpu().numpy(), a_o)
     close(qm.cpu().numpy(), q_o, what="qmax")
     close(hd.cpu().numpy().ravel(), z_o.ravel(), what="head")
-    print("near ties", orc.near_ties)
+    stats = {}
+    check_near_ties(orc, stats)
+    log_stats(f"q_forward_cfg{cfgk}_mode{mode}", stats)
 
 
 def test_explicit_equals_pruned_full_size():
@@ -92,50 +113,128 @@ def test_config4_pruned_q_forward_sampled():
     # config 4 space + net (W=64, Cmax=4, 4x512, P=256): pruned exact argmax vs the oracle's
     # pruned argmax on oracle-computed heads
     cfg, pool, osp, sess, orc = make_pair(4, 64, 64, argmax_mode=2)
-    orc.greedy_fn = lambda Fv, FcL, FcJ, s: PR.greedy_pruned(osp, Fv, FcL, FcJ, s, orc.off)
     wins, sched = _states(pool, 24, 64, 3)
     dw = torch.from_numpy(wins).to(sess.dev)
     ds = torch.from_numpy(sched.view(np.int64)).to(sess.dev)
     am, qm, hd = sess.q_forward(dw, ds, head=True)
     torch.cuda.synchronize()
     a_o, q_o, z_o = orc.q_forward(wins, sched, gpu_argmax=am.cpu().numpy())
+    orc.close()
     np.testing.assert_array_equal(am.cpu().numpy(), a_o)
     close(qm.cpu().numpy(), q_o, what="qmax")
     close(hd.cpu().numpy().ravel(), z_o.ravel(), what="head")
 
 
-def test_config2_full_size_step_sampled():
-    # BASELINE config 2 in the bench's launch configuration (E = B = 4096): one step + one
-    # update; a sample of envs is replayed through the oracle (per-env outputs depend only on
-    # that env's state and the shared weights)
-    from paper_2405_08754_b200.session import Session, streams_to_dev
-    cfg = synth.config(2)
+def test_double_dqn_hand_computed_through_libhrp():
+    # the hand-computed double-DQN case of tests/test_oracle_dqn.py
+    # through the C ABI: online and target heads differ, gamma = 0.9, s' not terminal
+    from test_oracle_dqn import (DDQN_ASTAR, DDQN_DELTA, DDQN_DQDZ, DDQN_LOSS,
+                                 DDQN_Z_ONLINE, DDQN_Z_TARGET, _hand_dqn_weights)
+    from paper_2405_08754_b200.session import Session
+    cfg = synth.config(1).with_(space=synth.SpaceCfg(3, 1, (50,), mig=False),
+                                net=synth.NetCfg(1, 4), gamma=0.9, lr=0.01)
     pool = synth.make_pool(27)
-    osp = SP.build_space(16, 3, cfg.space.shares)
-    th = synth.init_weights(QN.net_dims(osp, cfg.net))
-    E = cfg.n_envs
-    sess = Session(cfg, pool, init_weights=th)
-    win0 = synth.make_windows(pool, E, 16)
-    sess.reset(win0)
-    st = synth.step_streams(0, E, E, 16, pool)
-    thr = synth.eps_threshold(60, cfg.n_decay)   # late schedule: mostly greedy
-    dst = streams_to_dev(st, sess.dev)
-    sess.step(thr, dst["u_explore"], dst["u_action"], dst["next_windows"])
-    sess.update(dst["u_replay"], False)
+    osp = SP.build_space(3, 1, (50,), False)
+    dims, th_on, th_tg = _hand_dqn_weights(osp, cfg.net, DDQN_Z_ONLINE, DDQN_Z_TARGET)
+    sess = Session(cfg, pool, n_envs=1, batch=1, init_weights=th_on.astype(np.float32),
+                   replay=64)
+    from paper_2405_08754_b200 import hrp
+    hrp.hrp_set_weights(sess.ctx, np.concatenate([th_on, th_tg]).astype(np.float32))
+    d = sess.dev
+    sess.reset(np.array([[4, 11, 20]], np.uint8))
+    sess.step(1 << 32, torch.zeros(1, dtype=torch.int32, device=d),
+              torch.zeros(1, dtype=torch.int64, device=d), torch.zeros((1, 3), dtype=torch.uint8,
+                                                                       device=d))
+    sess.update(torch.zeros(1, dtype=torch.int32, device=d), False)
     sess.sync()
-    loss = sess.loss.item()
-    assert np.isfinite(loss)
-    pick = np.array([0, 1, 2, 777, 2048, 4095])
-    orc = EV.OracleDQN(osp, pool, cfg.net, th, len(pick), 1, 1 << 10, gamma=cfg.gamma,
-                       lr=cfg.lr)
-    orc.reset(win0[pick])
-    g = sess.greedy.cpu().numpy()[pick]
-    a, r, d, cr, q = orc.env_step(thr, st["u_explore"][pick], st["u_action"][pick],
-                                  st["next_windows"][pick], gpu_actions=g)
-    np.testing.assert_array_equal(sess.actions.cpu().numpy()[pick], a)
-    np.testing.assert_array_equal(sess.corun.cpu().numpy()[pick], cr)
-    close(sess.rewards.cpu().numpy()[pick], r, what="rewards")
-    close(sess.qsel.cpu().numpy()[pick], q, what="qsel")
+    assert int(sess.actions.item()) == 0 and int(sess.done.item()) == 0
+    assert float(sess.rewards.item()) == 0.0
+    assert int(sess.astar.item()) == DDQN_ASTAR
+    assert abs(sess.loss.item() - DDQN_LOSS) <= 1e-6
+    w = sess.weights()
+    n = sess.n_params
+    H = osp.H
+    gb = DDQN_DELTA * np.array(DDQN_DQDZ)
+    np.testing.assert_allclose(w[n - H:n], np.array(DDQN_Z_ONLINE) - 0.01 * gb, atol=1e-6)
+    np.testing.assert_allclose(w[2 * n - H:], DDQN_Z_TARGET, atol=0)   # target untouched
+    sess.close()
+
+
+def test_sharded_update_two_contexts_matches_oracle_simulation():
+    # E_local envs per rank, gradient = (sum over ranks of the local sums) /
+    # B_global.  Two world-1 contexts stand in for two ranks on one GPU: each exports its shard's
+    # gradient (hrp_dqn_grad, scale 1/B_local), the test averages them (the allreduce) and both
+    # apply it (hrp_apply_grad); the oracle simulates the same two shards (as in
+    # tests/test_parallel_gloo.py).  Replicas must stay identical and match the oracle.
+    from paper_2405_08754_b200.parallel import env_shard
+    from paper_2405_08754_b200.session import Session, streams_to_dev
+    cfg = synth.config(1)
+    pool = synth.make_pool(27)
+    osp = SP.build_space(4, 2, cfg.space.shares)
+    th = synth.init_weights(QN.net_dims(osp, cfg.net))
+    EL, WORLD, STEPS = 24, 2, 6
+    sess = [Session(cfg, pool, n_envs=EL, batch=EL, init_weights=th, replay=1024)
+            for _ in range(WORLD)]
+    orcs = [EV.OracleDQN(osp, pool, cfg.net, th, EL, EL, 1024, gamma=cfg.gamma, lr=cfg.lr)
+            for _ in range(WORLD)]
+    for r in range(WORLD):
+        w0 = synth.make_windows(pool, EL, 4, rank=r, first_env=env_shard(EL, r))
+        sess[r].reset(w0)
+        orcs[r].reset(w0)
+    n = sess[0].n_params
+    grads = [torch.empty(n, dtype=torch.float32, device=sess[0].dev) for _ in range(WORLD)]
+    for t in range(STEPS):
+        thr = synth.eps_threshold(t, cfg.n_decay)
+        sync_t = (t + 1) % 3 == 0
+        g_orc = 0
+        for r in range(WORLD):
+            st = synth.step_streams(t, EL, EL, 4, pool, rank=r, first_env=env_shard(EL, r))
+            d = streams_to_dev(st, sess[r].dev)
+            sess[r].step(thr, d["u_explore"], d["u_action"], d["next_windows"])
+            sess[r].grad(d["u_replay"], grads[r])
+            sess[r].sync()
+            a, *_ = orcs[r].env_step(thr, st["u_explore"], st["u_action"], st["next_windows"],
+                                     gpu_actions=sess[r].greedy.cpu().numpy())
+            np.testing.assert_array_equal(sess[r].actions.cpu().numpy(), a)
+            out = orcs[r].dqn_update(st["u_replay"], False, gpu_astar=sess[r].astar.cpu().numpy(),
+                                     b_total=EL * WORLD, apply=False)
+            close([sess[r].loss.item()], [out["loss"]], what=f"loss r={r} t={t}")
+            # this rank's exported gradient is its local sum / B_local
+            close(grads[r].cpu().numpy(), out["grad"] * WORLD, what=f"grad r={r} t={t}")
+            g_orc = g_orc + out["grad"]
+        g = (grads[0] + grads[1]) / WORLD          # the allreduce-sum scaled to 1 / B_global
+        for r in range(WORLD):
+            sess[r].apply_grad(g, sync_t)
+            orcs[r].apply(g_orc, sync_t)
+    w0, w1 = sess[0].weights(), sess[1].weights()
+    assert np.array_equal(w0, w1), "replicas diverged"
+    close(w0[:n], orcs[0].theta, what="online weights")
+    close(w0[n:], orcs[0].theta_t, what="target weights")
+    assert not np.allclose(w0[:n], th), "weights did not move"
+    for s in sess:
+        s.close()
+
+
+def test_non_finite_weights_are_reported_not_followed():
+    # NaN head outputs must not drive the env off its valid actions; hrp_sync reports
+    from paper_2405_08754_b200 import hrp
+    from paper_2405_08754_b200.session import streams_to_dev
+    cfg, pool, osp, sess, orc = make_pair(1, 16, 16, argmax_mode=1, workers=0)
+    orc.close()
+    w = sess.weights()
+    w[:] = np.nan
+    hrp.hrp_set_weights(sess.ctx, w)
+    sess.reset(synth.make_windows(pool, 16, 4))
+    st = streams_to_dev(synth.step_streams(0, 16, 16, 4, pool), sess.dev)
+    sess.step(0, st["u_explore"], st["u_action"], st["next_windows"])   # greedy only
+    with pytest.raises(hrp.HrpError) as ei:
+        sess.sync()
+    assert ei.value.status == hrp.HRP_ENUMERIC
+    a = sess.actions.cpu().numpy()
+    from oracle import actions as A
+    assert (a >= 0).all() and (a < A.n_actions(osp)).all()
+    sess.sync()                                   # the flag is cleared once reported
+    sess.close()
 
 
 def test_cuda_graph_replay_equals_eager():

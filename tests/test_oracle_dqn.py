@@ -150,6 +150,66 @@ def test_tabular_update_rule_special_case():
         assert q1 == pytest.approx(q0 + alpha * (y - q0), rel=1e-10, abs=1e-10)
 
 
+def _hand_dqn_weights(sp, net, z_online, z_target):
+    """One hidden layer of width 4 with zero weights and bias 1 (h = ReLU(1) = 1 for every
+    state), a zero head matrix and the head bias set to z: the head output is exactly z,
+    independent of the state, so every Q value below is a hand computation."""
+    dims = QN.net_dims(sp, net)
+    fin, w, H = dims
+    def flat(z):
+        return np.concatenate([np.zeros(w * fin), np.ones(w), np.zeros(H * w),
+                               np.asarray(z, np.float64)])
+    return dims, flat(z_online), flat(z_target)
+
+
+# Hand-computed double-DQN case (PAPER.md:180 "double DQN", :242 "duelling double DQN",
+# van Hasselt [45] at :382; update rule :178).  W = 3, Cmax = 1, MIG off: one layout (the
+# whole GPU), one slot type, H = 1 + 1 + 3 = 5, z = [v, aL, aJ0, aJ1, aJ2].
+#   online z = [0, 0, 0, 2, 1]   -> cJ = [-1, 1, 0]
+#   target z = [0.5, 0, 0, 0, 3] -> cJ = [-1, -1, 2], v = 0.5
+# Step: explore with k = 0 -> action 0 = job 0 alone; s' has jobs 1, 2 unscheduled; not done.
+# A single job on the whole GPU runs at its solo time: ratio 1, r = 0 (P:245, P:258).
+#   a*          = argmax_a Q_online(s', a) = job 1 (Q_online = 1 vs 0)
+#   y (double)  = r + gamma Q_target(s', a*) = 0 + 0.9 * (0.5 - 1)       = -0.45
+#   (plain DQN  r + gamma max_a Q_target(s', a) = 0.9 * 2.5 = 2.25;
+#    online-evaluated r + gamma Q_online(s', a*) = 0.9 * 1 = 0.9: both must NOT come out)
+#   Q(s, a)     = 0 + 0 + cJ[0] = -1;  delta = -1 - (-0.45) = -0.55;  L = delta^2 / 2 = 0.15125
+#   dQ/dz(a)    = [1, 1 - 1/L = 0, 1 - 1/3, -1/3, -1/3]  (Q4 structured gradient), B = 1,
+#   so the head bias moves by -lr * delta * dQ/dz and every head-matrix column (h = 1) alike.
+DDQN_Z_ONLINE = [0.0, 0.0, 0.0, 2.0, 1.0]
+DDQN_Z_TARGET = [0.5, 0.0, 0.0, 0.0, 3.0]
+DDQN_Y, DDQN_DELTA, DDQN_LOSS, DDQN_ASTAR = -0.45, -0.55, 0.15125, 1
+DDQN_DQDZ = [1.0, 0.0, 2.0 / 3.0, -1.0 / 3.0, -1.0 / 3.0]
+
+
+def test_double_dqn_target_hand_computed():
+    sp = SP.build_space(3, 1, (50,), False)
+    assert (sp.L, sp.T, sp.H) == (1, 1, 5)
+    pool = synth.make_pool(27)
+    net = NetCfg(1, 4)
+    dims, th_on, th_tg = _hand_dqn_weights(sp, net, DDQN_Z_ONLINE, DDQN_Z_TARGET)
+    lr = 0.01
+    ag = EV.OracleDQN(sp, pool, net, th_on, 1, 1, 64, gamma=0.9, lr=lr)
+    ag.theta_t = th_tg.copy()
+    ag.reset([[4, 11, 20]])
+    a, r, d, cr, q = ag.env_step(1 << 32, [0], [0], [[0, 0, 0]])   # explore, k = 0
+    assert int(a[0]) == 0 and int(d[0]) == 0 and r[0] == 0.0
+    assert q[0] == pytest.approx(-1.0, abs=1e-15)
+    out = ag.dqn_update([0], False)
+    assert int(out["astar"][0]) == DDQN_ASTAR
+    assert out["y"][0] == pytest.approx(DDQN_Y, abs=1e-12)
+    assert out["q_sa"][0] == pytest.approx(-1.0, abs=1e-12)
+    assert out["loss"] == pytest.approx(DDQN_LOSS, abs=1e-12)
+    H, w, fin = sp.H, 4, dims[0]
+    o_head = w * fin + w
+    gW = out["grad"][o_head:o_head + H * w].reshape(H, w)
+    gb = out["grad"][o_head + H * w:]
+    np.testing.assert_allclose(gb, DDQN_DELTA * np.array(DDQN_DQDZ), atol=1e-12)
+    np.testing.assert_allclose(gW, np.repeat(gb[:, None], w, 1), atol=1e-12)
+    assert not out["grad"][:o_head].any()          # zero head matrix: no hidden gradient
+    np.testing.assert_allclose(ag.theta[-H:], np.array(DDQN_Z_ONLINE) - lr * gb, atol=1e-15)
+
+
 def test_gamma_zero_target_is_reward():
     ag, sp, pool = _agent(E=8, B=8, gamma=0.0)
     for t in range(3):
