@@ -31,11 +31,15 @@ METRIC = "DQN env-steps/sec + Q-evals/sec at 1/2/4/8 B200; fraction of roofline"
 UNIT = "env-steps/s"
 
 
-def workload_name(cfg):
+def workload_name(cfg, E=None, B=None, scaling="weak"):
     s = cfg.space
+    E = cfg.n_envs if E is None else E
+    B = cfg.batch if B is None else B
+    shard = (f"E={cfg.n_envs} envs, B={cfg.batch} global, sharded ({E} / {B} per GPU)"
+             if scaling == "strong" else f"E={E} envs, B={B} per GPU")
     return (f"cfg{cfg.name[-1]}: W={s.window} jobs, Cmax={s.cmax}, MIG GI/CI x MPS "
             f"{{{min(s.shares)}..{max(s.shares)}}}%, Q-MLP {cfg.net.hidden_layers}x"
-            f"{cfg.net.hidden_width}, E={cfg.n_envs} envs, B={cfg.batch} per GPU")
+            f"{cfg.net.hidden_width}, {shard}")
 
 
 def dist_env():
@@ -46,13 +50,13 @@ def dist_env():
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_baseline(cfg, seconds=15.0):
-    """The oracle as it stands, single-threaded, on a bounded sample of the workload."""
-    try:
-        from threadpoolctl import threadpool_limits
-        lim = threadpool_limits(1)
-    except Exception:
-        lim = None
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def _oracle_rate(cfg, E, seconds, workers):
+    """env-steps/s of the oracle (env step + DQN update, explicit argmax over every valid
+    action, eps late in the schedule) on E envs, BLAS on one thread per process."""
     from oracle import env as EV
     from oracle import qnet as QN
     from oracle import space as SP
@@ -60,11 +64,13 @@ def cpu_baseline(cfg, seconds=15.0):
     sc = cfg.space
     osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
     th = synth.init_weights(QN.net_dims(osp, cfg.net))
-    E = 32
-    orc = EV.OracleDQN(osp, pool, cfg.net, th, E, E, 1 << 12, gamma=cfg.gamma, lr=cfg.lr)
+    orc = EV.OracleDQN(osp, pool, cfg.net, th, E, E, 1 << 12, gamma=cfg.gamma, lr=cfg.lr,
+                       workers=workers)
     orc.reset(synth.make_windows(pool, E, sc.window))
-    t0 = time.perf_counter()
+    if workers > 1:
+        orc.q_forward(orc.windows[:2], orc.sched[:2])     # start the worker processes untimed
     steps = 0
+    t0 = time.perf_counter()
     while True:
         st = synth.step_streams(steps, E, E, sc.window, pool)
         orc.env_step(synth.eps_threshold(60, cfg.n_decay), st["u_explore"], st["u_action"],
@@ -74,14 +80,37 @@ def cpu_baseline(cfg, seconds=15.0):
         if time.perf_counter() - t0 > seconds:
             break
     dt = time.perf_counter() - t0
-    if lim is not None:
-        lim.unregister() if hasattr(lim, "unregister") else None
-    return {"value": E * steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{steps} oracle steps of cfg{cfg.name[-1]} at E=B={E} (env step + DQN "
-                      f"update, explicit argmax over every valid action), 1 thread, {dt:.1f} s"}
+    orc.close()
+    return E * steps / dt, steps, dt
+
+
+def cpu_baseline(cfg, seconds=15.0):
+    """The oracle as it stands on a bounded sample of the workload, on this box's host cores:
+    all-core mode (the per-state argmax mapped over one process per core, BLAS 1 thread) as the
+    reported value, single-thread mode beside it."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    cores = host_cores()
+    v1, n1, t1 = _oracle_rate(cfg, 32, seconds / 2, 0)
+    Ea = max(32, 8 * cores)
+    va, na, ta = _oracle_rate(cfg, Ea, seconds / 2, cores)
+    name = f"cfg{cfg.name[-1]}"
+    return {"value": va, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{na} oracle steps of {name} at E=B={Ea} (env step + DQN update, explicit "
+                      f"argmax over every valid action mapped over {cores} processes), "
+                      f"{ta:.1f} s",
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1,
+                              "sample": f"{n1} oracle steps at E=B=32, 1 thread, {t1:.1f} s"}}
 
 
 def run_reference(args, cfg):
+    """The reference arm: the oracle as it stands (there is no reference implementation to
+    install, /root/reference holds only the paper) on this box's host cores, each step a
+    bounded sample (E = B = 16 envs) of the workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -93,12 +122,14 @@ def run_reference(args, cfg):
         threadpool_limits(1)
     except Exception:
         pass
+    cores = host_cores()
     pool = synth.make_pool(cfg.pool)
     sc = cfg.space
     osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
     th = synth.init_weights(QN.net_dims(osp, cfg.net))
     E = 16
-    orc = EV.OracleDQN(osp, pool, cfg.net, th, E, E, 1 << 12, gamma=cfg.gamma, lr=cfg.lr)
+    orc = EV.OracleDQN(osp, pool, cfg.net, th, E, E, 1 << 12, gamma=cfg.gamma, lr=cfg.lr,
+                       workers=cores)
     orc.reset(synth.make_windows(pool, E, sc.window))
 
     def step(t):
@@ -113,14 +144,16 @@ def run_reference(args, cfg):
     for t in range(args.steps):
         step(args.warmup + t)
     dt = time.perf_counter() - t0
+    orc.close()
     v = E * args.steps / dt
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": workload_name(cfg),
                                            "sample": f"E=B={E} envs per step (oracle)"},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"E=B={E} per step, {args.steps} steps, 1 thread"},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"E=B={E} per step, {args.steps} steps, argmax mapped over "
+                                      f"{cores} processes"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -241,9 +274,15 @@ def run_gpu(args, cfg):
     tab = hrp.hrp_layout_table(space_of(sc))           # host tables from libhrp
     osp = TableInfo(sc, tab)
     th = synth.init_weights(osp.dims(cfg.net))
-    E, B = cfg.n_envs, cfg.batch
+    if args.scaling == "strong":
+        # config 4: the global E = B = 65,536 sharded across the ranks
+        assert cfg.n_envs % world == 0 and cfg.batch % world == 0
+        E, B = cfg.n_envs // world, cfg.batch // world
+    else:
+        E, B = cfg.n_envs, cfg.batch                     # per rank (weak scaling)
     with torch.cuda.stream(stream):
-        sess = Session(cfg, pool, init_weights=th, device=local, rank=rank, world=world,
+        sess = Session(cfg, pool, n_envs=E, batch=B, init_weights=th, device=local, rank=rank,
+                       world=world,
                        nccl_id=nccl_id, argmax_mode=args.argmax, stream=stream)
         sess.reset(synth.make_windows(pool, E, sc.window, rank=rank,
                                        first_env=parallel.env_shard(E, rank)))
@@ -275,7 +314,8 @@ def run_gpu(args, cfg):
         if args.graph:
             # one CUDA graph per timed step (each step's inputs live at their own addresses and
             # the context's host counters -- step t, replay fill -- advance as the launches are
-            # recorded), replayed once each, in capture order
+            # recorded), replayed once each, in capture order.  With world > 1 the per-layer
+            # NCCL allreduces are captured into the same graph.
             for k in range(args.steps):
                 t = args.warmup + k
                 g = torch.cuda.CUDAGraph()
@@ -316,7 +356,7 @@ def run_gpu(args, cfg):
         hrp.hrp_profile(sess.ctx, False)
     # max over ranks
     ms = parallel.max_over_ranks(ms, dev)
-    value = world * E * args.steps / (ms / 1e3)
+    value = world * E * args.steps / (ms / 1e3)     # all ranks' env-steps / slowest rank's time
 
     # ---- e2e: host pinned streams copied in, results copied out, inside the timed region
     with torch.cuda.stream(stream):
@@ -399,9 +439,10 @@ def run_gpu(args, cfg):
     if rank == 0:
         res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                "dtype": "f32+i64", "data": "synthetic",
-               "config": {"workload": workload_name(cfg), "global_envs": world * E,
+               "config": {"workload": workload_name(cfg, E, B, args.scaling),
+                          "global_envs": world * E, "envs_per_gpu": E, "batch_per_gpu": B,
                           "actions_per_state": int(sess_actions(osp)),
                           "argmax": "explicit" if sess_explicit(args, sc) else "pruned-exact",
                           "gemm": "tcgen05 3xTF32 (fp32-accurate), TMA + TMEM",
@@ -421,7 +462,7 @@ def run_gpu(args, cfg):
                        "d2h_bytes_per_step": int(d2h)},
                "clocks": clk,
                "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
-        rl = rooflines(prof, args.steps, evals_k, cfg, osp)
+        rl = rooflines(prof, args.steps, evals_k, cfg, osp, E, B, burst=at_max_clock(clk))
         res["roofline"] = dominant(rl, args.config)
         tot = sum(v["ms_per_step"] for v in rl.values())
         res["roofline"]["share_of_step"] = rl[res["roofline"]["kernel"]]["ms_per_step"] / tot
@@ -460,18 +501,59 @@ def _peaks():
         return {}
 
 
-def rooflines(prof, steps, evals, cfg, osp):
+def at_max_clock(clk):
+    """True when NVML saw the SM clock at its maximum with no throttle reason during the timed
+    region: the burst peaks apply (B200_PROFILING.md), else the sustained ones."""
+    if not clk:
+        return False
+    return clk["sm_mhz"] >= 0.97 * clk["sm_max_mhz"] and not clk["reasons"]
+
+
+def tensor_peak(burst=True):
+    """fp32-accurate tensor-core peak of the 3xTF32 GEMMs (TFLOP/s, logical fp32 products) and
+    where it comes from: the measured cuBLAS TF32 peak (profiles/measured_peaks_r2.json,
+    tools/measure_peaks.py) / 3 MMAs per product, else MEASURED_PEAKS bf16 x 1/2 (the guide's
+    nominal TF32 : BF16 ratio) / 3."""
+    own = _own_peaks()
+    key = "tf32_tflops" if burst else "tf32_tflops_sustained"
+    if own.get(key):
+        return own[key] / 3.0, (f"measured cuBLAS TF32 {'burst' if burst else 'sustained'} "
+                                f"(profiles/measured_peaks_r2.json) x 1/3 (3xTF32 MMAs per product)")
+    pk = _peaks()
+    bf = float(pk.get("bf16_tflops" if burst else "bf16_tflops_sustained", 1653.9))
+    return bf / 2.0 / 3.0, (f"MEASURED_PEAKS bf16_tflops{'' if burst else '_sustained'} x 1/2 "
+                            "(tf32 ratio) x 1/3 (3xTF32 MMAs per product)")
+
+
+def alu_peak_tops():
+    """INT32/FP32 lane-op peak (T lane-ops/s): the measured microbenchmark when committed, else
+    148 SMs x 128 lanes x sm_max_mhz."""
+    own = _own_peaks()
+    if own.get("alu_tops"):
+        return own["alu_tops"], "measured IADD3 microbenchmark (profiles/measured_peaks_r2.json)"
+    pk = _peaks()
+    return (148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12,
+            "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)")
+
+
+def _own_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "measured_peaks_r2.json")))
+    except Exception:
+        return {}
+
+
+def rooflines(prof, steps, evals, cfg, osp, E=None, B=None, burst=True):
     """Per kernel class: achieved vs peak.  `evals` = (select, td)
     explicit Q-evaluations over the timed steps; prof = {class: (ms, launches)}."""
     pk = _peaks()
-    clock = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
-    alu_peak = 148 * 128 * clock / 1e12                     # T lane-ops/s
-    tf32 = float(pk.get("bf16_tflops_sustained", 1407.2)) / 2.0
-    fp32_tc = tf32 / 3.0                                    # 3xTF32: three MMAs per product
+    alu_peak, alu_src = alu_peak_tops()
+    fp32_tc, tc_src = tensor_peak(burst)
     hbm = float(pk.get("hbm_gbs", 6453.7))
     dims = [osp.W * 17] + [cfg.net.hidden_width] * cfg.net.hidden_layers + [osp.H]
     F = sum(2 * dims[i] * dims[i + 1] for i in range(len(dims) - 1))
-    E, B = cfg.n_envs, cfg.batch
+    E = cfg.n_envs if E is None else E
+    B = cfg.batch if B is None else B
     out = {}
     head_struct = prof.get("head_bwd", (0.0, 0))[1] > 0
     for name, (ms, cnt) in prof.items():
@@ -486,7 +568,7 @@ def rooflines(prof, steps, evals, cfg, osp):
                        frac=ach / alu_peak, work=f"{n / steps:.4g} Q-evals/step (valid actions covered) x 2 lane-ops "
                             "(one add forming the score, one compare), the naive algorithm's "
                             "cost",
-                       peak_src="148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)")
+                       peak_src=alu_src)
         elif name in ("gemm_fwd", "gemm_bwd"):
             rows = E + 3 * B if name == "gemm_fwd" else B
             if name == "gemm_fwd":
@@ -508,8 +590,7 @@ def rooflines(prof, steps, evals, cfg, osp):
             ach = flops * steps / sec / 1e12
             per.update(bound="tensor", achieved=ach, peak=fp32_tc, unit="TFLOP/s",
                        frac=ach / fp32_tc, work=f"{flops / 1e9:.4g} GFLOP/step (logical fp32)",
-                       peak_src="MEASURED_PEAKS bf16_tflops_sustained x 1/2 (tf32 ratio) x 1/3 "
-                                "(3xTF32 MMAs per fp32 product)")
+                       peak_src=tc_src)
         elif name == "encode":
             rows = E + 2 * B
             byts = rows * (osp.W * 17 * 4 + osp.W + 8)
@@ -604,8 +685,11 @@ def run_brute(args, cfg):
         rgs = torch.empty((n, W), dtype=torch.uint8, device=dev)
         bact = torch.empty((n, W), dtype=torch.int64, device=dev)
 
+        # the resident plan: tables uploaded once, each call only enqueues the search kernel
+        plan = hrp.hrp_brute_create(space, prof, local, stream.cuda_stream)
+
         def call():
-            hrp.hrp_bruteforce_optimum(space, prof, n, w, best, solo, rgs, bact, stream.cuda_stream)
+            hrp.hrp_brute_run(plan, n, w, best, solo, rgs, bact, stream.cuda_stream)
         clocks = Clocks(local)
         ms = _timed_calls(call, args.steps, args.warmup, stream, flush)
         clk = clocks.stop()
@@ -620,6 +704,8 @@ def run_brute(args, cfg):
             oh[0].copy_(best, non_blocking=True)
             oh[1].copy_(rgs, non_blocking=True)
         ms_e2e = _timed_calls(call_e2e, args.steps, 1, stream, flush)
+        stream.synchronize()
+        hrp.hrp_brute_destroy(plan)
     # algorithmic work: (job set, layout, slot permutation) evaluations of phase 1
     from math import comb, factorial
     nc = np.bincount(np.asarray(tab["nslots"]), minlength=5)
@@ -629,8 +715,7 @@ def run_brute(args, cfg):
     slot_terms = sum(comb(W, c) * int(nc[c]) * factorial(c) * 2 * c for c in range(1, 5))
     sec = ms / 1e3
     value = n * args.steps / sec
-    pk = _peaks()
-    alu_peak = 148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    alu_peak, alu_src = alu_peak_tops()
     ach = slot_terms * n * args.steps / sec / 1e12
     res = {"metric": "brute-force optimum windows/s (BASELINE config 3)", "value": value,
            "unit": "windows/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -651,7 +736,7 @@ def run_brute(args, cfg):
                         "traffic": measured_traffic("brute")[0],
                         "work": f"{slot_terms} CoRun terms per window (2C per (set, layout, "
                                 f"sigma) evaluation, one lane-op each; {evals} evaluations)",
-                        "peak_src": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)"}}
+                        "peak_src": alu_src}}
     if not args.no_cpu_baseline:
         from oracle import brute as BR
         from oracle import space as SP
@@ -687,11 +772,10 @@ def run_infer(args, cfg):
     chunk = 65536
     base = synth.config(2)
     ecfg = base.with_(n_envs=chunk, batch=chunk)
-    from oracle import qnet as QN
-    from oracle import space as SP
+    from paper_2405_08754_b200.session import space_of
     sc = cfg.space
-    osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
-    th = synth.init_weights(QN.net_dims(osp, cfg.net))
+    osp = TableInfo(sc, hrp.hrp_layout_table(space_of(sc)))    # sizes from libhrp's tables
+    th = synth.init_weights(osp.dims(cfg.net))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):
         sess = Session(ecfg, pool, init_weights=th, device=local, stream=stream, replay=chunk)
@@ -765,13 +849,14 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the timed steps eagerly instead of from per-step CUDA graphs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="weak: E per GPU fixed (default, configs 1-2); strong: the config's "
+                         "global E and B sharded over the GPUs (default for config 4)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        # per-step graphs are verified on one GPU only (tests/test_gpu_dqn.py); with NCCL inside
-        # the step the multi-rank run launches eagerly
-        args.graph = False
+    if args.scaling is None:
+        args.scaling = "strong" if args.config == 4 else "weak"
     cfg = synth.config(args.config)
     if args.impl == "reference":
         run_reference(args, cfg)

@@ -205,6 +205,11 @@ hrp_status hrp_decode_action(const hrp_space *space, int64_t idx, int32_t *l, in
                              int32_t slot_of[4]);
 
 int64_t hrp_n_params(const hrp_ctx *ctx);  /* parameters of ONE network, -1 if ctx NULL */
+/* Test hook: rows [0, rows) of hidden layer `layer`'s output (0-based, ReLU applied) from the
+ * most recent online forward, as the backward's ReLU' mask reads them (tf32 hi plane: same sign
+ * as the fp32 value) -> d_out f32 [rows][w] (device).  After hrp_dqn_update / hrp_dqn_grad the
+ * rows [0, B) are the sampled states s.  Used by the parity tests for reading R25. */
+hrp_status hrp_get_hidden(hrp_ctx *ctx, int layer, int64_t rows, float *d_out);
 int32_t hrp_head_width(const hrp_ctx *ctx); /* H */
 /* Host copies of the flat fp32 weights: out [2 * n_params] = online | target. */
 hrp_status hrp_get_weights(hrp_ctx *ctx, float *out);
@@ -244,6 +249,11 @@ hrp_status hrp_eval_counts(hrp_ctx *ctx, int64_t *out);
 hrp_status hrp_diag_gemm(int device, void *cuda_stream, int M, int N, int K, const float *d_A,
                          const float *d_W, const float *d_bias, float *d_D,
                          uint64_t *d_trace, int reps, int force_bn, float *ms_out);
+/* Diagnostics (process-wide, for A/B measurements): key 0 = TMEM accumulator layout of the
+ * tensor-core GEMMs: 0 one accumulator for all three 3xTF32 products, 1 the hi.hi products in
+ * one accumulator and the hi.lo + lo.hi corrections in another, 2 (default) the hi.hi products
+ * spread round-robin by K block over up to three accumulators plus the correction one. */
+hrp_status hrp_diag_config(int key, int value);
 /* Block until the context's stream is idle; returns any pending CUDA/NCCL error, or
  * HRP_ENUMERIC (once, then cleared) if a greedy argmax since the last call met non-finite Q
  * values (e.g. diverged weights); such a state took its lowest valid action instead. */

@@ -34,6 +34,7 @@ from . import pruned as PR
 from . import qnet as QN
 
 NEAR_TIE = 1e-4  # reading R15: argmax mismatch allowed iff oracle gap <= 1e-4 max(1, |Q|)
+RELU_NEAR = 1e-4  # reading R25: ReLU' decision may differ iff |pre-activation| <= 1e-4 rms
 
 
 class Tables:
@@ -168,6 +169,8 @@ class OracleDQN:
         self.near_ties = 0       # GPU argmax adopted under R15 (oracle gap within the window)
         self.near_tie_gap = 0.0  # largest adopted gap, in units of max(1, |Q|)
         self.greedy_calls = 0    # greedy argmaxes taken (the population near_ties is out of)
+        self.relu_near = 0       # ReLU' decisions adopted under R25
+        self.relu_decisions = 0  # ReLU' decisions compared (hidden units x samples)
 
     # -- helpers -----------------------------------------------------------------------
     def close(self):
@@ -192,10 +195,32 @@ class OracleDQN:
             return self._procs.map(_worker_call, items, chunksize=ch)
         return [self.greedy_fn(*it) for it in items]
 
-    def _heads(self, theta, windows, scheds):
+    def _heads(self, theta, windows, scheds, pre=None):
         X = np.stack([encode(w, int(s), self.pool, self.sp.W) for w, s in zip(windows, scheds)])
-        z, acts = QN.forward(theta, self.dims, X)
+        z, acts = QN.forward(theta, self.dims, X, pre)
         return z, acts
+
+    def _adopt_masks(self, pre, gpu_masks):
+        """Reading R25 (the R15 lockstep for ReLU'): the backward's mask [pre > 0] is decided in
+        floating point; where the GPU's decision differs and the oracle's pre-activation is
+        within RELU_NEAR x rms(layer) of zero, the oracle takes the GPU's decision (counted).
+        Any other difference fails."""
+        masks = []
+        for l, (y, g) in enumerate(zip(pre, gpu_masks)):
+            m = y > 0
+            g = np.asarray(g, bool).reshape(m.shape)
+            diff = m != g
+            self.relu_decisions += m.size
+            if diff.any():
+                band = RELU_NEAR * max(1e-30, float(np.sqrt(np.mean(y ** 2))))
+                far = diff & (np.abs(y) > band)
+                if far.any():
+                    b, j = np.argwhere(far)[0]
+                    raise AssertionError(f"ReLU mask mismatch layer {l} sample {b} unit {j}: "
+                                         f"oracle pre-activation {y[b, j]:.3e}, band {band:.3e}")
+                self.relu_near += int(diff.sum())
+            masks.append(g)
+        return masks
 
     def _adopt(self, mine, theirs, Fv, FcL, FcJ, qmax, sched):
         """Near-tie lockstep (reading R15): adopt the GPU's action if our Q^ gap <= 1e-4."""
@@ -283,10 +308,12 @@ class OracleDQN:
         nf = min(self.N, self.inserted)
         return np.array([(int(u) * nf) >> 32 for u in u_replay], np.int64)
 
-    def dqn_update(self, u_replay, sync_target, gpu_astar=None, b_total=None, apply=True):
+    def dqn_update(self, u_replay, sync_target, gpu_astar=None, b_total=None, apply=True,
+                   gpu_masks=None):
         """One double-DQN step on a replay batch.  Returns a dict with loss, idx, a*, y,
         Q(s,a), grad (sum-form / B_total).  With apply=False the caller applies the SGD
-        step (multi-rank simulation)."""
+        step (multi-rank simulation).  gpu_masks: the GPU's ReLU' decisions of the s rows per
+        hidden layer (bool [B][w]) for the near-zero lockstep of reading R25."""
         sp, B = self.sp, len(u_replay)
         b_total = b_total or B
         idx = self.sample(u_replay)
@@ -298,7 +325,8 @@ class OracleDQN:
         dec = [A.decode(sp, int(a), self.off) for a in act]
         sch2 = np.array([int(s) | A.group_mask(g) for s, (_, g, _) in zip(sch, dec)],
                         np.uint64)
-        z_s, acts = self._heads(self.theta, win, sch)
+        pre = []
+        z_s, acts = self._heads(self.theta, win, sch, pre)
         z_n, _ = self._heads(self.theta, win, sch2)
         z_t, _ = self._heads(self.theta_t, win, sch2)
         astar = np.full(B, -1, np.int64)
@@ -330,7 +358,8 @@ class OracleDQN:
             dz[b] = QN.dq_dz(sp, l, g, sg) * (q_sa[b] - y[b]) / b_total
         delta = q_sa - y
         loss = float((delta ** 2).sum() / (2 * B))
-        grad = QN.backward(self.theta, self.dims, acts, dz)
+        masks = self._adopt_masks(pre, gpu_masks) if gpu_masks is not None else None
+        grad = QN.backward(self.theta, self.dims, acts, dz, masks)
         if apply:
             self.apply(grad, sync_target)
         return {"loss": loss, "idx": idx, "astar": astar, "y": y, "q_sa": q_sa,

@@ -47,20 +47,24 @@ def unflatten(theta, dims):
     return out
 
 
-def forward(theta, dims, x):
-    """x [M][in] -> (z [M][H], acts) where acts[l] is the input of layer l."""
+def forward(theta, dims, x, pre=None):
+    """x [M][in] -> (z [M][H], acts) where acts[l] is the input of layer l.  If `pre` is a
+    list, the hidden layers' pre-activations are appended to it."""
     layers = unflatten(np.asarray(theta, np.float64), dims)
     h = np.asarray(x, np.float64)
     acts = []
     for i, (Wm, b) in enumerate(layers):
         acts.append(h)
         y = h @ Wm.T + b
+        if i < len(layers) - 1 and pre is not None:
+            pre.append(y)
         h = np.maximum(y, 0.0) if i < len(layers) - 1 else y
     return h, acts
 
 
-def backward(theta, dims, acts, dz):
-    """Gradient of sum(dz * z) w.r.t. the flat parameters."""
+def backward(theta, dims, acts, dz, masks=None):
+    """Gradient of sum(dz * z) w.r.t. the flat parameters.  ReLU'(h) = [h > 0] for the input of
+    layer i > 0, or masks[i - 1] when given (the near-zero lockstep of reading R25)."""
     layers = unflatten(np.asarray(theta, np.float64), dims)
     grads = [None] * len(layers)
     d = np.asarray(dz, np.float64)
@@ -69,7 +73,7 @@ def backward(theta, dims, acts, dz):
         h = acts[i]
         grads[i] = (d.T @ h, d.sum(0))
         if i > 0:
-            d = (d @ Wm) * (h > 0)
+            d = (d @ Wm) * (h > 0 if masks is None else masks[i - 1])
     return np.concatenate([np.concatenate([gw.ravel(), gb]) for gw, gb in grads])
 
 

@@ -152,6 +152,10 @@ struct TcArgs {
   float* DT;               // optional D^T [N][ldt] for rows < t_rows (split: hi -> DT, lo -> DTlo)
   float* DTlo;
   int ldt, t_rows;
+  // accumulators in TMEM (BN columns each): nmain for the hi.hi products (k-block kb goes to
+  // main accumulator kb % nmain) + one for the correction terms hi.lo + lo.hi when ncorr = 1;
+  // summed in fp32 in the epilogue.  tmem_cols = the power-of-two allocation.
+  int nmain, ncorr, tmem_cols;
   unsigned long long* trace;  // diagnostics: per-event timestamps of CTA (0,0,0), or null
 };
 
@@ -219,7 +223,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(a.tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -250,19 +254,27 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32<BN>();
+      // the tensor core's accumulation truncates (profiles/r2_gemm_precision.txt): spreading
+      // the hi.hi products over nmain accumulators and keeping the 2^-11-smaller correction
+      // terms out of them shortens each accumulator's chain of truncated adds
+      const uint32_t t_corr = tmem + (uint32_t)(a.nmain * BN);
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         mbar_wait(&full_bar[s], (kb / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint64_t dah = smem_desc(a_hi(s)), dal = smem_desc(a_lo(s));
         const uint64_t dbh = smem_desc(b_hi(s)), dbl = smem_desc(b_lo(s));
+        const int mi = kb % a.nmain;
+        const uint32_t t_main = tmem + (uint32_t)(mi * BN);
+        const uint32_t t_c = a.ncorr ? t_corr : t_main;
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
           const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // 32 B per K=8 step
-          const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
-          mma_tf32(tmem, dah + adv, dbh + adv, idesc, acc0);
-          mma_tf32(tmem, dah + adv, dbl + adv, idesc, 1u);
-          mma_tf32(tmem, dal + adv, dbh + adv, idesc, 1u);
+          const uint32_t accm = (kb >= a.nmain || k > 0) ? 1u : 0u;
+          const uint32_t accc = a.ncorr ? ((kb > 0 || k > 0) ? 1u : 0u) : 1u;
+          mma_tf32(t_main, dah + adv, dbh + adv, idesc, accm);
+          mma_tf32(t_c, dah + adv, dbl + adv, idesc, accc);
+          mma_tf32(t_c, dal + adv, dbh + adv, idesc, 1u);
         }
         mma_commit(&empty_bar[s]);
         if (kb < 64) TRACE(130 + kb);
@@ -313,6 +325,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
       uint32_t v[32];
       TMEM_LD32(trow + c, v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      {
+        // sum of the accumulators in fp32 (round to nearest): mains in order, then corrections
+        const int nm = min(a.nmain, nk);
+        for (int q2 = 1; q2 < nm + a.ncorr; ++q2) {
+          const int slot = q2 < nm ? q2 : a.nmain;
+          uint32_t u[32];
+          TMEM_LD32(trow + (uint32_t)(slot * BN) + c, u);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(u[j]));
+        }
+      }
       const int col = n0 + c + lane;
       float mk[32];
       if (EPI == TC_EPI_RELU_MASK) {           // all 32 mask loads in flight at once
@@ -357,7 +381,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   __syncthreads();
   if (threadIdx.x == 0) TRACE(195);
   if (warp == 2) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(a.tmem_cols));
   }
 }
 
@@ -512,9 +537,19 @@ bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int ld, int bo
   return true;
 }
 
+int g_acc_mode = 2;   // 0: one accumulator; 1: main + correction; 2: up to 3 mains + correction
+
 template <int BN, int STAGES, int EPI>
 hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   CUtensorMap ma0, ma1, mb0, mb1;
+  a.ncorr = g_acc_mode >= 1 ? 1 : 0;
+  a.nmain = g_acc_mode >= 2 ? std::max(1, std::min(3, 512 / BN - 1)) : 1;
+  {
+    const int need = (a.nmain + a.ncorr) * BN;
+    int cols = 32;
+    while (cols < need) cols <<= 1;
+    a.tmem_cols = cols;
+  }
   // boxes never exceed the tensor; rows of a tile beyond the box only feed masked outputs
   a.boxA = std::min(BM, a.M);
   a.boxB = std::min(BN, a.N);
@@ -676,6 +711,7 @@ hrp_status tc_rowsum(TcGemm* g, cudaStream_t st, int rows, int cols, Planes src,
 }
 
 void tc_gemm_force_bn(int bn) { g_force_bn = bn; }
+void tc_gemm_set_acc_mode(int m) { g_acc_mode = m < 0 ? 0 : (m > 2 ? 2 : m); }
 
 int tc_gemm_launches(TcGemm* g) {
   int n = g->launches;

@@ -44,6 +44,9 @@ hrp_status tc_transpose(TcGemm* g, cudaStream_t st, int rows, int cols, int ld_s
 hrp_status tc_rowsum(TcGemm* g, cudaStream_t st, int rows, int cols, Planes src, float* out);
 // diagnostics: force the output tile width (64 / 128 / 256; 0 = heuristic)
 void tc_gemm_force_bn(int bn);
+// diagnostics: TMEM accumulator layout (0 one accumulator, 1 main + corrections, 2 up to three
+// round-robin mains + corrections; default 2)
+void tc_gemm_set_acc_mode(int mode);
 int tc_gemm_launches(TcGemm* g);
 const char* tc_gemm_error();
 }  // namespace hrp

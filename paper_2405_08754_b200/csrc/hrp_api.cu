@@ -1286,6 +1286,17 @@ hrp_status hrp_eval_counts(hrp_ctx* c, int64_t* out) {
   return HRP_OK;
 }
 
+hrp_status hrp_get_hidden(hrp_ctx* c, int layer, int64_t rows, float* d_out) {
+  if (!c || !d_out) return fail(HRP_EINVAL, "NULL argument");
+  if (layer < 0 || layer >= (int)c->act.size()) return fail(HRP_ERANGE, "layer out of range");
+  if (rows < 0 || rows > c->rows_max) return fail(HRP_ERANGE, "rows out of range");
+  CK(cudaSetDevice(c->device));
+  const size_t w = (size_t)c->dims[layer + 1];
+  CK(cudaMemcpyAsync(d_out, c->act[layer].hi, sizeof(float) * w * (size_t)rows,
+                     cudaMemcpyDeviceToDevice, c->stream));
+  return HRP_OK;
+}
+
 int64_t hrp_n_params(const hrp_ctx* c) { return c ? c->n_params : -1; }
 int32_t hrp_head_width(const hrp_ctx* c) { return c ? c->hs.head_width() : -1; }
 int64_t hrp_launch_count(const hrp_ctx* c) { return c ? c->launches : -1; }
@@ -1354,6 +1365,14 @@ hrp_status hrp_diag_gemm(int device, void* cuda_stream, int M, int N, int K, con
   tc_gemm_destroy(g);
   if (s) return fail(s, tc_gemm_error());
   return HRP_OK;
+}
+
+hrp_status hrp_diag_config(int key, int value) {
+  if (key == 0) {
+    tc_gemm_set_acc_mode(value);
+    return HRP_OK;
+  }
+  return fail(HRP_EINVAL, "unknown diagnostic key");
 }
 
 hrp_status hrp_sync(hrp_ctx* c) {

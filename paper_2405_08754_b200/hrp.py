@@ -75,11 +75,14 @@ def lib():
             "hrp_layout_table": [P, i32, P, P, P, P, P, P],
             "hrp_decode_action": [P, i64, P, P, P],
             "hrp_get_weights": [P, P],
+            "hrp_get_hidden": [P, S, i64, P],
             "hrp_set_weights": [P, P],
             "hrp_sync": [P],
             "hrp_profile": [P, S],
             "hrp_profile_read": [P, P, P],
             "hrp_eval_counts": [P, P],
+            "hrp_diag_config": [S, S],
+            "hrp_diag_gemm": [S, P, S, S, S, P, P, P, P, P, S, S, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -265,6 +268,10 @@ def hrp_get_weights(ctx):
     return out
 
 
+def hrp_get_hidden(ctx, layer, rows, d_out):
+    _check(lib().hrp_get_hidden(ctx, int(layer), int(rows), _ptr(d_out)))
+
+
 def hrp_set_weights(ctx, w):
     w = np.ascontiguousarray(w, np.float32)
     _check(lib().hrp_set_weights(ctx, _hptr(w)))
@@ -293,6 +300,19 @@ def hrp_eval_counts(ctx):
     out = np.zeros(2, np.int64)
     _check(lib().hrp_eval_counts(ctx, _hptr(out)))
     return int(out[0]), int(out[1])
+
+
+def hrp_diag_config(key, value):
+    _check(lib().hrp_diag_config(int(key), int(value)))
+
+
+def hrp_diag_gemm(device, cuda_stream, M, N, K, d_A, d_W, d_bias, d_D, reps=0, force_bn=0):
+    """D = A . W^T + bias through the 3xTF32 GEMM; returns the average ms of `reps` launches."""
+    ms = C.c_float(0.0)
+    _check(lib().hrp_diag_gemm(int(device), C.c_void_p(cuda_stream), int(M), int(N), int(K),
+                               _ptr(d_A), _ptr(d_W), _ptr(d_bias), _ptr(d_D), None, int(reps),
+                               int(force_bn), C.byref(ms)))
+    return ms.value
 
 
 def hrp_sync(ctx):

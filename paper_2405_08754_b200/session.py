@@ -92,6 +92,19 @@ class Session:
         hrp.hrp_q_forward(self.ctx, n, windows, sched, am, qm, hd)
         return am, qm, hd
 
+    def relu_masks(self, rows=None):
+        """The backward's ReLU' decisions of the last update's s rows, per hidden layer (bool
+        numpy [rows][w]); test hook for reading R25."""
+        rows = self.B if rows is None else rows
+        out = []
+        for l in range(self.cfg.net.hidden_layers):
+            t = torch.empty((rows, self.cfg.net.hidden_width), dtype=torch.float32,
+                            device=self.dev)
+            hrp.hrp_get_hidden(self.ctx, l, rows, t)
+            torch.cuda.synchronize(self.dev)
+            out.append((t > 0).cpu().numpy())
+        return out
+
     def weights(self):
         return hrp.hrp_get_weights(self.ctx)
 
