@@ -249,6 +249,10 @@ hrp_status hrp_eval_counts(hrp_ctx *ctx, int64_t *out);
 hrp_status hrp_diag_gemm(int device, void *cuda_stream, int M, int N, int K, const float *d_A,
                          const float *d_W, const float *d_bias, float *d_D,
                          uint64_t *d_trace, int reps, int force_bn, float *ms_out);
+/* Diagnostics: ALU issue-rate microbenchmark on `device` -- 148 x 8 CTAs of 256 threads, each
+ * thread 8 independent chains of `iters` x 16 fp32 adds (is_int = 0) or int32 adds (1);
+ * *lane_ops_per_s = adds / second (the roofline peak of the selection kernels). */
+hrp_status hrp_diag_alu(int device, int is_int, int iters, double *lane_ops_per_s);
 /* Diagnostics (process-wide, for A/B measurements): key 0 = TMEM accumulator layout of the
  * tensor-core GEMMs: 0 one accumulator for all three 3xTF32 products, 1 the hi.hi products in
  * one accumulator and the hi.lo + lo.hi corrections in another, 2 (default) the hi.hi products

@@ -995,9 +995,8 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   sample_encode_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(
       c->dt.sp, c->dt.pool, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r,
       c->rep_done, c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx, c->X.hi, c->X.lo,
-      c->ldX);
+      c->ldX, c->XT.hi, c->XT.lo, c->Bp);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
-  if ((s = transpose(c, HRP_K_ENCODE, B, c->dims[0], c->ldX, c->X, c->XT, c->Bp))) return s;
   // online net on [s; s'] (activations of the s rows kept for backward) on the main stream,
   // target net on s' beside it (its own activation scratch)
   const bool conc = concurrent(c);
@@ -1364,6 +1363,70 @@ hrp_status hrp_diag_gemm(int device, void* cuda_stream, int M, int N, int K, con
   cudaFreeAsync(split, st);
   tc_gemm_destroy(g);
   if (s) return fail(s, tc_gemm_error());
+  return HRP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// ALU peak microbenchmark: 8 independent dependency chains of fp32 adds (FADD) or int32 adds
+// (IADD3) per thread; the chains keep every issue slot fed.
+template <bool INT>
+__global__ void __launch_bounds__(256) alu_kernel(int iters, float seed, float* out) {
+  float f[8];
+  uint32_t u[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    f[j] = seed * (float)(threadIdx.x + j);
+    u[j] = (uint32_t)threadIdx.x * 2654435761u + j;
+  }
+  const float df = seed * 1e-7f;
+  const uint32_t du = (uint32_t)__float_as_uint(seed) | 1u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (INT) asm volatile("add.u32 %0, %0, %1;" : "+r"(u[j]) : "r"(du));
+        else asm volatile("add.f32 %0, %0, %1;" : "+f"(f[j]) : "f"(df));
+      }
+    }
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc += INT ? (float)u[j] : f[j];
+  if (acc == 1234.5f) out[0] = acc;   // keeps the chains live
+}
+}  // namespace
+
+extern "C" {
+
+hrp_status hrp_diag_alu(int device, int is_int, int iters, double* lane_ops_per_s) {
+  if (!lane_ops_per_s || iters < 1) return fail(HRP_EINVAL, "bad argument");
+  CK(cudaSetDevice(device));
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  float* out = nullptr;
+  CK(cudaMalloc(&out, 16));
+  const int grid = nsm * 8, block = 256;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto run = [&]() {
+    if (is_int) alu_kernel<true><<<grid, block>>>(iters, 1.0001f, out);
+    else alu_kernel<false><<<grid, block>>>(iters, 1.0001f, out);
+  };
+  run();   // warm-up
+  CK(cudaEventRecord(e0));
+  run();
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  *lane_ops_per_s = (double)grid * block * (double)iters * 16.0 * 8.0 / (ms * 1e-3);
   return HRP_OK;
 }
 

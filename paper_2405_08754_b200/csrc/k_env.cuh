@@ -11,8 +11,10 @@ namespace hrp {
 
 // ---------------------------------------------------------------------------------------
 // a2: x[row] = W rows of [features(12) | c/cbar, m/mbar, T/Tbar | scheduled | U/W]
-// One warp per state.
-// X is written raw, or (Xlo != NULL) split into tf32 hi / lo planes for the tensor-core GEMMs.
+// One warp per state: lane j builds job j's 17 values in a per-warp shared-memory row (odd
+// stride, conflict-free; the 12 features as three 16-byte loads), then the warp copies the
+// row out with 16-byte coalesced stores, split into the tf32 hi / lo planes the GEMMs read.
+constexpr int kEncMaxIn = 64 * 17;           // W <= 64
 
 // Window means as the reciprocal scales W / sum (the ratios of P:240 / R10), warp-wide.
 __device__ __forceinline__ void window_scales(int W, const uint8_t* __restrict__ w,
@@ -38,46 +40,65 @@ __device__ __forceinline__ void window_scales(int W, const uint8_t* __restrict__
   iT = fW / (float)sT;
 }
 
-// One state's row of X (warp-wide) from its window, scheduled mask and window scales.
-__device__ __forceinline__ void encode_row(int W, const uint8_t* __restrict__ w, uint64_t s,
-                                           float ic, float im, float iT, const DevPool& pool,
-                                           float* __restrict__ x, float* __restrict__ xl) {
+// One state's row (warp-wide) into the 16-byte-aligned shared row `r` [W * 17].
+__device__ __forceinline__ void encode_row_smem(int W, const uint8_t* __restrict__ w, uint64_t s,
+                                                float ic, float im, float iT,
+                                                const DevPool& pool, float* __restrict__ r) {
   const int lane = threadIdx.x & 31;
-  const int in = W * 17;
-  const int U = W - __popcll(s);
-  const float fW = (float)W;
-#pragma unroll 4
-  for (int i = lane; i < in; i += 32) {   // unrolled: 4 independent load chains in flight
-    const int j = i / 17, col = i - j * 17;
+  const float uw = (float)(W - __popcll(s)) / (float)W;
+  for (int j = lane; j < W; j += 32) {
     const int p = w[j];
-    float v;
-    if (col < 12) v = pool.feat[p * 12 + col];
-    else if (col == 12) v = (float)pool.c[p] * ic;
-    else if (col == 13) v = (float)pool.m[p] * im;
-    else if (col == 14) v = (float)pool.T[p] * iT;
-    else if (col == 15) v = (float)((s >> j) & 1ull);
-    else v = (float)U / fW;
-    if (xl) {
-      const float h = tf32_rna(v);
-      x[i] = h;
-      xl[i] = v - h;
-    } else {
-      x[i] = v;
-    }
+    const float4* f4 = reinterpret_cast<const float4*>(pool.feat + p * 12);
+    const float4 a = f4[0], b = f4[1], c = f4[2];
+    float* q = r + j * 17;
+    q[0] = a.x; q[1] = a.y; q[2] = a.z; q[3] = a.w;
+    q[4] = b.x; q[5] = b.y; q[6] = b.z; q[7] = b.w;
+    q[8] = c.x; q[9] = c.y; q[10] = c.z; q[11] = c.w;
+    q[12] = (float)pool.c[p] * ic;
+    q[13] = (float)pool.m[p] * im;
+    q[14] = (float)pool.T[p] * iT;
+    q[15] = (float)((s >> j) & 1ull);
+    q[16] = uw;
   }
+  __syncwarp();
 }
 
-__global__ void encode_kernel(int M, int W, const uint8_t* __restrict__ win,
-                              const uint64_t* __restrict__ sched, DevPool pool,
-                              float* __restrict__ X, float* __restrict__ Xlo, int ldx) {
-  const int warps = blockDim.x >> 5;
-  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
-    const uint8_t* w = win + (size_t)row * W;
-    float ic, im, iT;
-    window_scales(W, w, pool, ic, im, iT);
-    encode_row(W, w, sched[row], ic, im, iT, pool, X + (size_t)row * ldx,
-               Xlo ? Xlo + (size_t)row * ldx : nullptr);
+// A shared row of n floats to global as tf32 hi / lo planes x, xl (16-byte aligned), warp-wide.
+__device__ __forceinline__ float4 rna4(float4 v) {
+  return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+}
+__device__ __forceinline__ void store_row(const float* __restrict__ r, int n, float* __restrict__ x,
+                                          float* __restrict__ xl) {
+  const int lane = threadIdx.x & 31;
+  const int n4 = n >> 2;
+  for (int i = lane; i < n4; i += 32) {
+    const float4 v = reinterpret_cast<const float4*>(r)[i];
+    const float4 h = rna4(v);
+    reinterpret_cast<float4*>(x)[i] = h;
+    reinterpret_cast<float4*>(xl)[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
   }
+  for (int i = 4 * n4 + lane; i < n; i += 32) {
+    const float h = tf32_rna(r[i]);
+    x[i] = h;
+    xl[i] = r[i] - h;
+  }
+  __syncwarp();
+}
+
+// grid ceil(M / 8) x 256 threads (one warp per state).
+__global__ void __launch_bounds__(256) encode_kernel(int M, int W, const uint8_t* __restrict__ win,
+                                                     const uint64_t* __restrict__ sched, DevPool pool,
+                                                     float* __restrict__ X, float* __restrict__ Xlo,
+                                                     int ldx) {
+  __shared__ __align__(16) float rows[8][kEncMaxIn];
+  const int warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * 8 + warp;
+  if (row >= M) return;
+  const uint8_t* w = win + (size_t)row * W;
+  float ic, im, iT;
+  window_scales(W, w, pool, ic, im, iT);
+  encode_row_smem(W, w, sched[row], ic, im, iT, pool, rows[warp]);
+  store_row(rows[warp], W * 17, X + (size_t)row * ldx, Xlo + (size_t)row * ldx);
 }
 
 // Permutations of 0..C-1 in lexicographic (= Lehmer rank) order, packed 2 bits per entry.
@@ -199,22 +220,25 @@ struct SelArgs {
 // idx_b = floor(u_b * n_filled / 2^32), gathers the transition into the batch buffers and
 // encodes both of its states -- row b (s: window, scheduled mask) and row B + b (s': the same
 // window with the action's jobs scheduled; the select kernel stores that mask beside s at
-// insert time) -- sharing the window scales.  Same arithmetic as encode_kernel over the 2B
-// rows; one launch and one pass over the window.
-__global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restrict__ u,
-                                     int64_t n_filled, const uint8_t* __restrict__ rep_win,
-                                     const uint64_t* __restrict__ rep_sched,
-                                     const int64_t* __restrict__ rep_act,
-                                     const float* __restrict__ rep_r,
-                                     const uint8_t* __restrict__ rep_done, uint8_t* __restrict__ bwin,
-                                     uint64_t* __restrict__ bsched, int64_t* __restrict__ bact,
-                                     float* __restrict__ br, uint8_t* __restrict__ bdone,
-                                     int64_t* __restrict__ out_idx, float* __restrict__ X,
-                                     float* __restrict__ Xlo, int ldx) {
-  const int warps = blockDim.x >> 5;
+// insert time) -- sharing the window scales.  The CTA's 8 consecutive samples also write the
+// s rows transposed, XT [in][ldt] (the first layer's weight-gradient operand, hi / lo planes): 8 samples x one
+// input column = one 32-byte sector per store group.  grid ceil(B / 8) x 256 threads.
+__global__ void __launch_bounds__(256)
+sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restrict__ u,
+                     int64_t n_filled, const uint8_t* __restrict__ rep_win,
+                     const uint64_t* __restrict__ rep_sched, const int64_t* __restrict__ rep_act,
+                     const float* __restrict__ rep_r, const uint8_t* __restrict__ rep_done,
+                     uint8_t* __restrict__ bwin, uint64_t* __restrict__ bsched,
+                     int64_t* __restrict__ bact, float* __restrict__ br,
+                     uint8_t* __restrict__ bdone, int64_t* __restrict__ out_idx,
+                     float* __restrict__ X, float* __restrict__ Xlo, int ldx,
+                     float* __restrict__ XT, float* __restrict__ XTlo, int ldt) {
+  __shared__ __align__(16) float rows[8][kEncMaxIn];
+  const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int W = sp.W;
-  for (int b = blockIdx.x * warps + (threadIdx.x >> 5); b < B; b += gridDim.x * warps) {
+  const int W = sp.W, in = W * 17;
+  const int b0 = blockIdx.x * 8, b = b0 + warp;
+  if (b < B) {
     const int64_t idx = (int64_t)(((uint64_t)u[b] * (uint64_t)n_filled) >> 32);
     const uint8_t* w = rep_win + idx * W;
     const uint64_t s = rep_sched[2 * idx], s2 = rep_sched[2 * idx + 1];
@@ -233,10 +257,21 @@ __global__ void sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uin
     }
     float ic, im, iT;
     window_scales(W, w, pool, ic, im, iT);
-    encode_row(W, w, s, ic, im, iT, pool, X + (size_t)b * ldx,
-               Xlo ? Xlo + (size_t)b * ldx : nullptr);
-    encode_row(W, w, s2, ic, im, iT, pool, X + (size_t)(B + b) * ldx,
-               Xlo ? Xlo + (size_t)(B + b) * ldx : nullptr);
+    // s' first (row B + b), then s, whose shared row stays for the transposed store
+    encode_row_smem(W, w, s2, ic, im, iT, pool, rows[warp]);
+    store_row(rows[warp], in, X + (size_t)(B + b) * ldx, Xlo + (size_t)(B + b) * ldx);
+    encode_row_smem(W, w, s, ic, im, iT, pool, rows[warp]);
+    store_row(rows[warp], in, X + (size_t)b * ldx, Xlo + (size_t)b * ldx);
+  }
+  __syncthreads();
+  const int nb = min(8, B - b0);
+  for (int e = threadIdx.x; e < in * 8; e += blockDim.x) {
+    const int i = e >> 3, bb = e & 7;
+    if (bb < nb) {
+      const float v = rows[bb][i], h = tf32_rna(v);
+      XT[(size_t)i * ldt + b0 + bb] = h;
+      XTlo[(size_t)i * ldt + b0 + bb] = v - h;
+    }
   }
 }
 

@@ -82,6 +82,7 @@ def lib():
             "hrp_profile_read": [P, P, P],
             "hrp_eval_counts": [P, P],
             "hrp_diag_config": [S, S],
+            "hrp_diag_alu": [S, S, S, P],
             "hrp_diag_gemm": [S, P, S, S, S, P, P, P, P, P, S, S, P],
         }
         for name, args in sig.items():
@@ -300,6 +301,12 @@ def hrp_eval_counts(ctx):
     out = np.zeros(2, np.int64)
     _check(lib().hrp_eval_counts(ctx, _hptr(out)))
     return int(out[0]), int(out[1])
+
+
+def hrp_diag_alu(device, is_int, iters=4096):
+    v = C.c_double(0.0)
+    _check(lib().hrp_diag_alu(int(device), int(is_int), int(iters), C.byref(v)))
+    return v.value
 
 
 def hrp_diag_config(key, value):
