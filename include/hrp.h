@@ -91,6 +91,13 @@ typedef struct {
   int32_t argmax_mode;      /* 0 auto (= 2), 1 explicit enumeration of every valid action  */
                             /* (W <= 16), 2 exact top-C pruned search; same actions bit    */
                             /* for bit (R15)                                    */
+  /* SURVEY §8(f) row 4 variants (zero = the paper's defaults):                            */
+  int32_t optimizer;        /* 0 plain SGD, 1 Adam (Kingma & Ba) with the three      */
+  float adam_beta1, adam_beta2, adam_eps;   /* parameters below (bias-corrected moments)    */
+  int32_t loss;             /* 0 (1/2) delta^2, 1 Huber with threshold huber_kappa:  */
+  float huber_kappa;        /* h = delta^2/2 if |delta| <= kappa else kappa(|delta| - kappa/2) */
+  int32_t precision;        /* 0 fp32-accurate 3xTF32 GEMMs; 1 fast mode: one TF32 MMA per   */
+                            /* product (inputs rounded to tf32), policy-level parity only     */
 } hrp_train_cfg;
 
 /* ---- lifecycle ------------------------------------------------------------------------ */

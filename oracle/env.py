@@ -138,7 +138,8 @@ class OracleDQN:
 
     def __init__(self, space, pool, net, theta0, n_envs, batch, replay_capacity,
                  gamma=0.99, lr=1e-3, reward_lambda=0.0, q3=1, greedy=None, argmax="explicit",
-                 workers=0):
+                 workers=0, optimizer="sgd", adam=(0.9, 0.999, 1e-8), loss="squared",
+                 huber_kappa=1.0):
         self.sp = space
         self.pool = pool
         self.argmax = argmax
@@ -157,6 +158,12 @@ class OracleDQN:
         self.theta_t = self.theta.copy()
         self.E, self.B, self.N = n_envs, batch, replay_capacity
         self.gamma, self.lr, self.lam, self.q3 = gamma, lr, reward_lambda, q3
+        # Adam (Kingma & Ba, bias-corrected moments) instead of the plain
+        # SGD step, Huber instead of (1/2) delta^2 (P:178 states neither; both are variants)
+        self.optimizer, self.adam, self.loss_kind, self.kappa = optimizer, adam, loss, huber_kappa
+        self.adam_m = np.zeros_like(self.theta)
+        self.adam_v = np.zeros_like(self.theta)
+        self.adam_t = 0
         self.windows = None
         self.sched = None
         self.rep_win = np.zeros((self.N, space.W), np.uint8)
@@ -355,9 +362,9 @@ class OracleDQN:
             cL, cJ = QN.center(aL, aJ)
             l, g, sg = dec[b]
             q_sa[b] = QN.q_value(v, cL, cJ, sp, l, g, sg)
-            dz[b] = QN.dq_dz(sp, l, g, sg) * (q_sa[b] - y[b]) / b_total
+            dz[b] = QN.dq_dz(sp, l, g, sg) * self._dloss(q_sa[b] - y[b]) / b_total
         delta = q_sa - y
-        loss = float((delta ** 2).sum() / (2 * B))
+        loss = float(sum(self._loss_term(d) for d in delta) / B)
         masks = self._adopt_masks(pre, gpu_masks) if gpu_masks is not None else None
         grad = QN.backward(self.theta, self.dims, acts, dz, masks)
         if apply:
@@ -365,8 +372,31 @@ class OracleDQN:
         return {"loss": loss, "idx": idx, "astar": astar, "y": y, "q_sa": q_sa,
                 "grad": grad}
 
+    def _loss_term(self, d):
+        """(1/2) delta^2 (P:178), or Huber: delta^2 / 2 if |delta| <= kappa, else
+        kappa (|delta| - kappa / 2)."""
+        d = float(d)
+        if self.loss_kind == "huber" and abs(d) > self.kappa:
+            return self.kappa * (abs(d) - 0.5 * self.kappa)
+        return 0.5 * d * d
+
+    def _dloss(self, d):
+        """d(loss term)/d delta: delta, or clip(delta, -kappa, kappa) for Huber."""
+        if self.loss_kind == "huber":
+            return float(np.clip(d, -self.kappa, self.kappa))
+        return float(d)
+
     def apply(self, grad, sync_target):
-        self.theta = self.theta - self.lr * grad
+        if self.optimizer == "adam":
+            b1, b2, eps = self.adam
+            self.adam_t += 1
+            self.adam_m = b1 * self.adam_m + (1 - b1) * grad
+            self.adam_v = b2 * self.adam_v + (1 - b2) * grad * grad
+            mh = self.adam_m / (1 - b1 ** self.adam_t)
+            vh = self.adam_v / (1 - b2 ** self.adam_t)
+            self.theta = self.theta - self.lr * mh / (np.sqrt(vh) + eps)
+        else:
+            self.theta = self.theta - self.lr * grad
         if sync_target:
             self.theta_t = self.theta.copy()
 

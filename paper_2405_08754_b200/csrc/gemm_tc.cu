@@ -156,6 +156,7 @@ struct TcArgs {
   // main accumulator kb % nmain) + one for the correction terms hi.lo + lo.hi when ncorr = 1;
   // summed in fp32 in the epilogue.  tmem_cols = the power-of-two allocation.
   int nmain, ncorr, tmem_cols;
+  int fast;                // 1: one TF32 MMA per K step (hi . hi), lo planes not loaded
   unsigned long long* trace;  // diagnostics: per-event timestamps of CTA (0,0,0), or null
 };
 
@@ -238,16 +239,18 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(2 * (a.boxA + a.boxB)) * BK * 4;
+      const uint32_t bytes = (uint32_t)((a.fast ? 1 : 2) * (a.boxA + a.boxB)) * BK * 4;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty_bar[s], ((kb / STAGES) - 1) & 1);
         mbar_expect_tx(&full_bar[s], bytes);
         const int kk = kbeg + kb * BK;
         tma_load_2d(a_hi(s), &mapA0, &full_bar[s], kk, m0);
-        tma_load_2d(a_lo(s), &mapA1, &full_bar[s], kk, m0);
         tma_load_2d(b_hi(s), &mapB0, &full_bar[s], kk, n0);
-        tma_load_2d(b_lo(s), &mapB1, &full_bar[s], kk, n0);
+        if (!a.fast) {
+          tma_load_2d(a_lo(s), &mapA1, &full_bar[s], kk, m0);
+          tma_load_2d(b_lo(s), &mapB1, &full_bar[s], kk, n0);
+        }
         if (kb < 64) TRACE(2 + kb);
       }
     }
@@ -273,8 +276,10 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
           const uint32_t accm = (kb >= a.nmain || k > 0) ? 1u : 0u;
           const uint32_t accc = a.ncorr ? ((kb > 0 || k > 0) ? 1u : 0u) : 1u;
           mma_tf32(t_main, dah + adv, dbh + adv, idesc, accm);
-          mma_tf32(t_c, dah + adv, dbl + adv, idesc, accc);
-          mma_tf32(t_c, dal + adv, dbh + adv, idesc, 1u);
+          if (!a.fast) {
+            mma_tf32(t_c, dah + adv, dbl + adv, idesc, accc);
+            mma_tf32(t_c, dal + adv, dbh + adv, idesc, 1u);
+          }
         }
         mma_commit(&empty_bar[s]);
         if (kb < 64) TRACE(130 + kb);
@@ -542,7 +547,7 @@ int g_acc_mode = 2;   // 0: one accumulator; 1: main + correction; 2: up to 3 ma
 template <int BN, int STAGES, int EPI>
 hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   CUtensorMap ma0, ma1, mb0, mb1;
-  a.ncorr = g_acc_mode >= 1 ? 1 : 0;
+  a.ncorr = (g_acc_mode >= 1 && !a.fast) ? 1 : 0;
   a.nmain = g_acc_mode >= 2 ? std::max(1, std::min(3, 512 / BN - 1)) : 1;
   {
     const int need = (a.nmain + a.ncorr) * BN;
@@ -632,9 +637,10 @@ static hrp_status run_bn(int bn, cudaStream_t st, Planes A, Planes B, const TcAr
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, Planes A,
                        int lda, Planes B, int ldb, const float* bias, const float* aux, int ldaux,
                        float* D, float* Dlo, float* DT, float* DTlo, int t_rows,
-                       unsigned long long* trace) {
+                       unsigned long long* trace, int fast) {
   g->launches++;
   TcArgs a{};
+  a.fast = fast;
   a.trace = trace;
   a.M = M; a.N = N; a.K = K; a.kc = K;
   a.lda = lda; a.ldb = ldb;
@@ -648,7 +654,7 @@ hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K,
 }
 
 hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes A, Planes B,
-                         float* ws, size_t ws_elems, float* D, float* db) {
+                         float* ws, size_t ws_elems, float* D, float* db, int fast) {
   // D[M][N] = A[M][K] . B[N][K]^T, split-K + deterministic reduce
   const long tiles = (long)((M + BM - 1) / BM) * ((N + 127) / 128);
   // one wave: tiles x S <= SMs (each CTA holds one SM; a second partial wave costs a whole CTA
@@ -662,6 +668,7 @@ hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes
   TcArgs a{};
   a.M = M; a.N = N; a.K = K; a.kc = kc;
   a.lda = K; a.ldb = K;
+  a.fast = fast;
   a.D = (S > 1 || db) ? ws : D; a.ldd = N;
   g->launches++;
   hrp_status s = launch<128, 3, TC_EPI_STORE>(st, A, B, a, S);

@@ -26,13 +26,14 @@ inline int r4(int x) { return (x + 3) / 4 * 4; }
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, Planes A,
                        int lda, Planes B, int ldb, const float* bias, const float* aux, int ldaux,
                        float* D, float* Dlo, float* DT, float* DTlo, int t_rows,
-                       unsigned long long* trace = nullptr);
+                       unsigned long long* trace = nullptr, int fast = 0);
 // Weight gradient: D[M][N] = A[M][K] . B[N][K]^T (K % 4 == 0, dense rows), split-K over K with
 // a deterministic reduction through ws (>= S * M * N floats).  With db != NULL the last row of
 // B is a ones row (hi 1, lo 0): column N-1 of the product is the row sum of A (the bias
 // gradient), scattered to db[M], and D is [M][N-1].
 hrp_status tc_gemm_wgrad(TcGemm* g, cudaStream_t st, int M, int N, int K, Planes A, Planes B,
-                         float* ws, size_t ws_elems, float* D, float* db = nullptr);
+                         float* ws, size_t ws_elems, float* D, float* db = nullptr,
+                         int fast = 0);
 // hi/lo split of W [rows][cols] into planes of row stride round_up(cols, 4); optionally also of
 // W^T ([cols][rows], row stride round_up(rows, 4)) into hiT/loT.
 hrp_status tc_split(TcGemm* g, cudaStream_t st, int rows, int cols, const float* w, float* hi,

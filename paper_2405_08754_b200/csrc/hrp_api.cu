@@ -292,6 +292,8 @@ struct hrp_ctx {
   unsigned long long* n_evals = nullptr;
   unsigned* sched_ctr = nullptr;      // [4]: row schedulers of the select / TD kernels, tdq ticket
   unsigned* dev_err = nullptr;        // [1]: bit 0 = a greedy argmax found no comparable Q (NaN)
+  float *adam_m = nullptr, *adam_v = nullptr;   // Adam moments [n_params] (optimizer 1)
+  int64_t adam_t = 0;                 // Adam updates applied
   size_t p_smem = 0;   // warp-per-state selection / TD kernels
   int sel_variant = 0; // 0 pruned argmax, 1..4 explicit enumeration with Cmax = variant
   int p_grid = 0;
@@ -421,7 +423,8 @@ hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, Planes A, i
                   Pl D, Pl DT = Pl{}, int t_rows = 0) {
   prof_begin(c);
   hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, lda, Planes{Bh, Bl}, r4(K), bias,
-                             aux, ldaux, D.hi, D.lo, DT.hi, DT.lo, t_rows);
+                             aux, ldaux, D.hi, D.lo, DT.hi, DT.lo, t_rows, nullptr,
+                             c->cfg.precision == 1);
   if (s) return fail(s, tc_gemm_error());
   c->launches += tc_gemm_launches(c->tc) - 1;
   return launch_check(c, cls);
@@ -559,7 +562,7 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     auto wgrad = [&]() -> hrp_status {
       prof_begin(c);
       hrp_status t = tc_gemm_wgrad(c->tc, c->stream, fo, fi + 1, Bp, dYT.c(), HinT.c(), c->ws_splitk,
-                                   c->ws_splitk_elems, gW, gb);
+                                   c->ws_splitk_elems, gW, gb, c->cfg.precision == 1);
       if (t) return fail(t, tc_gemm_error());
       c->launches += tc_gemm_launches(c->tc) - 1;
       if ((t = launch_check(c, HRP_K_GEMM_BWD))) return t;
@@ -703,6 +706,15 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     return fail(HRP_ERANGE, "hidden_layers 1..8, hidden_width 4..1024 multiple of 4");
   if (!(cfg->lr >= 0.f) || !(cfg->gamma >= 0.f && cfg->gamma <= 1.f))
     return fail(HRP_EINVAL, "lr >= 0 and 0 <= gamma <= 1 required");
+  if (cfg->optimizer < 0 || cfg->optimizer > 1 || cfg->loss < 0 || cfg->loss > 1 ||
+      cfg->precision < 0 || cfg->precision > 1)
+    return fail(HRP_EINVAL, "optimizer, loss and precision must be 0 or 1");
+  if (cfg->optimizer == 1 && !(cfg->adam_beta1 >= 0.f && cfg->adam_beta1 < 1.f &&
+                               cfg->adam_beta2 >= 0.f && cfg->adam_beta2 < 1.f &&
+                               cfg->adam_eps > 0.f))
+    return fail(HRP_EINVAL, "Adam needs 0 <= beta1, beta2 < 1 and eps > 0");
+  if (cfg->loss == 1 && !(cfg->huber_kappa > 0.f))
+    return fail(HRP_EINVAL, "Huber loss needs huber_kappa > 0");
   std::unique_ptr<hrp_ctx> c(new hrp_ctx());
   try {
     std::string err;
@@ -841,6 +853,12 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->sched_ctr, 4 * sizeof(unsigned)));   // select, TD, tdq ticket
   CK(cudaMemsetAsync(c->sched_ctr, 0, 4 * sizeof(unsigned), c->stream));
   CK(ar.alloc((void**)&c->dev_err, sizeof(unsigned)));
+  if (cfg->optimizer == 1) {
+    CK(ar.alloc((void**)&c->adam_m, sizeof(float) * o));
+    CK(ar.alloc((void**)&c->adam_v, sizeof(float) * o));
+    CK(cudaMemsetAsync(c->adam_m, 0, sizeof(float) * o, c->stream));
+    CK(cudaMemsetAsync(c->adam_v, 0, sizeof(float) * o, c->stream));
+  }
   CK(cudaMemsetAsync(c->dev_err, 0, sizeof(unsigned), c->stream));
   if (init_weights) {
     CK(cudaMemcpyAsync(c->theta, init_weights, sizeof(float) * o, cudaMemcpyHostToDevice, c->stream));
@@ -1038,6 +1056,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   t.bdone = c->bdone;
   t.gamma = c->cfg.gamma;
   t.inv_btot = 1.f / ((float)B * (float)c->world);
+  t.huber_kappa = c->cfg.loss == 1 ? c->cfg.huber_kappa : 0.f;
   t.explicit_mode = c->explicit_mode;
   t.hdesc = c->hdesc;
   t.tdesc = c->tdesc;
@@ -1101,6 +1120,17 @@ hrp_status apply_grad(hrp_ctx* c, const float* grad, int sync_target) {
     g.fo[i] = c->dims[i + 1];
   }
   g.woff[g.nl] = c->n_params;
+  if (c->cfg.optimizer == 1) {
+    c->adam_t += 1;
+    g.adam = 1;
+    g.m = c->adam_m;
+    g.v = c->adam_v;
+    g.b1 = c->cfg.adam_beta1;
+    g.b2 = c->cfg.adam_beta2;
+    g.eps = c->cfg.adam_eps;
+    g.c1 = (float)(1.0 / (1.0 - std::pow((double)c->cfg.adam_beta1, (double)c->adam_t)));
+    g.c2 = (float)(1.0 / (1.0 - std::pow((double)c->cfg.adam_beta2, (double)c->adam_t)));
+  }
   sgd_split_kernel<<<8 * 148, 256, 0, c->stream>>>(g);
   return launch_check(c, HRP_K_SGD);
 }

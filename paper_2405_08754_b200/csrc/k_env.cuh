@@ -284,6 +284,7 @@ struct TdArgs {
   const uint8_t* bdone;
   float gamma;
   float inv_btot;       // 1 / (B * world)
+  float huber_kappa;    // > 0: Huber loss (dL/dQ = clip(delta, +-kappa)), 0: (1/2) delta^2
   bool explicit_mode;
   float* dsq;           // [B]
   int* tdesc;           // [B][8] descriptor of a* (word 2 = -1 when done)
@@ -334,12 +335,29 @@ struct SgdSplitArgs {
   int64_t woff[kMaxLayers + 1];      // flat offsets (woff[nl] = n)
   int64_t soff[kMaxLayers], soffT[kMaxLayers];
   int fi[kMaxLayers], fo[kMaxLayers];
+  // Adam (adam != 0): m = b1 m + (1 - b1) g, v = b2 v + (1 - b2) g^2,
+  // theta -= lr (m c1) / (sqrt(v c2) + eps) with the bias corrections c1 = 1/(1 - b1^t),
+  // c2 = 1/(1 - b2^t) of update t (host-computed)
+  int adam;
+  float* m;
+  float* v;
+  float b1, b2, eps, c1, c2;
 };
 
 __global__ void sgd_split_kernel(SgdSplitArgs a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float v = a.th[i] - a.lr * a.g[i];
+    float v;
+    if (a.adam) {
+      const float g = a.g[i];
+      const float m = a.b1 * a.m[i] + (1.f - a.b1) * g;
+      const float s = a.b2 * a.v[i] + (1.f - a.b2) * g * g;
+      a.m[i] = m;
+      a.v[i] = s;
+      v = a.th[i] - a.lr * (m * a.c1) / (sqrtf(s * a.c2) + a.eps);
+    } else {
+      v = a.th[i] - a.lr * a.g[i];
+    }
     a.th[i] = v;
     if (a.sync) a.tgt[i] = v;
     int l = 0;

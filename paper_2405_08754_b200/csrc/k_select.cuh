@@ -871,8 +871,14 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
                                 a.bo, a.c0o, a.mTo, a.w);
     const float delta = q - y;
     if (lane == 0) {
-      a.dsq[b] = delta * delta;
-      hd[0] = __float_as_int(delta * a.inv_btot);
+      // loss term 2 h(delta) (the loss is sum / (2B)) and the scaled dL/dQ
+      float g = delta, h2 = delta * delta;
+      if (a.huber_kappa > 0.f && fabsf(delta) > a.huber_kappa) {
+        g = copysignf(a.huber_kappa, delta);
+        h2 = 2.f * a.huber_kappa * (fabsf(delta) - 0.5f * a.huber_kappa);
+      }
+      a.dsq[b] = h2;
+      hd[0] = __float_as_int(g * a.inv_btot);
     }
   }
   if (a.loss == nullptr) return;

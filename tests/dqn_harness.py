@@ -64,7 +64,10 @@ def check_near_ties(orc, stats):
 
 
 def make_pair(cfgk, E, B, argmax_mode=2, lam=0.0, W=None, replay=None, workers=None,
-              oracle_argmax=None):
+              oracle_argmax=None, variant=None):
+    """variant: SURVEY §8(f)4 options for both sides, e.g. {"optimizer": "adam",
+    "loss": "huber", "huber_kappa": 10.0}."""
+    variant = dict(variant or {})
     from paper_2405_08754_b200.session import Session
     cfg = synth.config(cfgk)
     if W is not None:
@@ -78,7 +81,8 @@ def make_pair(cfgk, E, B, argmax_mode=2, lam=0.0, W=None, replay=None, workers=N
     theta0 = synth.init_weights(dims)
     N = replay or max(1 << 10, 4 * E)
     sess = Session(cfg, pool, n_envs=E, batch=B, init_weights=theta0, argmax_mode=argmax_mode,
-                   replay=N, reward_lambda=lam)
+                   replay=N, reward_lambda=lam, **variant)
+    variant.pop("precision", None)
     assert sess.n_params == len(theta0)
     # the oracle's argmax: explicit enumeration where it is cheap, else the exact top-C search
     # (oracle/pruned.py, pinned against explicit enumeration); both give the same index
@@ -86,25 +90,25 @@ def make_pair(cfgk, E, B, argmax_mode=2, lam=0.0, W=None, replay=None, workers=N
     nw = WORKERS if workers is None else workers
     orc = EV.OracleDQN(osp, pool, cfg.net, theta0, E, B, N, gamma=cfg.gamma, lr=cfg.lr,
                        reward_lambda=lam, argmax=argmax,
-                       workers=nw if (E > 64 or osp.W >= 16) else 0)
+                       workers=nw if (E > 64 or osp.W >= 16) else 0, **variant)
     return cfg, pool, osp, sess, orc
 
 
 def run_lockstep(cfgk, E, B, steps, argmax_mode=2, lam=0.0, W=None, seed_step=0,
                  check_weights_every=1, name=None, workers=None, oracle_argmax=None,
-                 resync=False, drift_min_steps=None):
+                 resync=False, drift_min_steps=None, variant=None):
     """drift_min_steps: free-running drift probe -- instead of failing, stop at the first step
     whose float outputs leave the tolerance, record it, and assert it is >= drift_min_steps."""
     from paper_2405_08754_b200.session import streams_to_dev
     t_start = time.time()
     cfg, pool, osp, sess, orc = make_pair(cfgk, E, B, argmax_mode, lam, W, workers=workers,
-                                          oracle_argmax=oracle_argmax)
+                                          oracle_argmax=oracle_argmax, variant=variant)
     Wn = osp.W
     win0 = synth.make_windows(pool, E, Wn, step=seed_step)
     sess.reset(win0)
     orc.reset(win0)
     stats = {"cfg": cfgk, "E": E, "B": B, "steps": steps, "argmax_mode": argmax_mode,
-             "oracle_argmax": orc.argmax, "resync": resync, "max_err": {}}
+             "oracle_argmax": orc.argmax, "resync": resync, "variant": variant, "max_err": {}}
     if resync:
         check_weights_every = 1
     n = sess.n_params

@@ -219,3 +219,45 @@ def test_gamma_zero_target_is_reward():
     st = synth.step_streams(9, ag.E, ag.B, sp.W, pool)
     out = ag.dqn_update(st["u_replay"], False)
     np.testing.assert_allclose(out["y"], ag.rep_r[out["idx"]], atol=0)
+
+
+def _hand_agent(**kw):
+    sp = SP.build_space(3, 1, (50,), False)
+    pool = synth.make_pool(27)
+    net = NetCfg(1, 4)
+    dims, th_on, th_tg = _hand_dqn_weights(sp, net, DDQN_Z_ONLINE, DDQN_Z_TARGET)
+    ag = EV.OracleDQN(sp, pool, net, th_on, 1, 1, 64, gamma=0.9, lr=0.01, **kw)
+    ag.theta_t = th_tg.copy()
+    ag.reset([[4, 11, 20]])
+    ag.env_step(1 << 32, [0], [0], [[0, 0, 0]])
+    return ag, sp
+
+
+def test_huber_loss_hand_computed():
+    # Huber with kappa = 0.25 on the hand case above (delta = -0.55):
+    # loss = kappa (|delta| - kappa/2) = 0.25 * 0.425 = 0.10625, dL/dQ = clip(delta) = -0.25;
+    # with kappa >= |delta| it is the squared loss (0.15125, dL/dQ = delta)
+    ag, sp = _hand_agent(loss="huber", huber_kappa=0.25)
+    out = ag.dqn_update([0], False)
+    assert out["loss"] == pytest.approx(0.10625, abs=1e-12)
+    gb = out["grad"][-sp.H:]
+    np.testing.assert_allclose(gb, -0.25 * np.array(DDQN_DQDZ), atol=1e-12)
+    ag2, _ = _hand_agent(loss="huber", huber_kappa=1.0)
+    out2 = ag2.dqn_update([0], False)
+    assert out2["loss"] == pytest.approx(DDQN_LOSS, abs=1e-12)
+
+
+def test_adam_first_step_is_lr_times_sign():
+    # Adam's first bias-corrected step is m^/(sqrt(v^) + eps) = g/(|g| + eps): every parameter
+    # with a nonzero gradient moves by lr * sign(-g) (Kingma & Ba, Sec. 2), zero-gradient ones
+    # stay; a second identical gradient moves them by the same amount again
+    ag, sp = _hand_agent(optimizer="adam", adam=(0.9, 0.999, 1e-12))
+    th0 = ag.theta.copy()
+    out = ag.dqn_update([0], False)
+    g = out["grad"]
+    step = ag.theta - th0
+    np.testing.assert_allclose(step, -0.01 * np.sign(g), atol=1e-9)
+    assert (step[g == 0] == 0).all()
+    th1 = ag.theta.copy()
+    ag.apply(g, False)
+    np.testing.assert_allclose(ag.theta - th1, -0.01 * np.sign(g), atol=1e-9)
