@@ -193,6 +193,15 @@ hrp_status hrp_brute_run(hrp_brute *plan, int64_t n_windows, const uint8_t *d_wi
                          int64_t *d_best_corun, int64_t *d_solo, uint8_t *d_rgs,
                          int64_t *d_block_action, void *cuda_stream);
 hrp_status hrp_brute_destroy(hrp_brute *plan);
+/* Per-job co-run times (AppSlowdown; Fairness) of given actions on the
+ * plan's space: for n (window uint8 [n][W], action int64 [n]) pairs, d_corun int64 [n] =
+ * CoRunTime and d_solo int64 [n] = SoloRunTime of the action's job set (R7, R8), and
+ * d_member_time int64 [n][4] = each member's own co-run time t_k -- member i is window position
+ * g_i (ascending, hrp_decode_action's order), -1 padded; AppSlowdown = t_k / T_p.  An action
+ * outside [0, |A|) gives -1 everywhere.  Asynchronous on cuda_stream. */
+hrp_status hrp_job_times(hrp_brute *plan, int64_t n, const uint8_t *d_windows,
+                         const int64_t *d_actions, int64_t *d_corun, int64_t *d_solo,
+                         int64_t *d_member_time, void *cuda_stream);
 
 /* ---- host helpers (no device work) ---------------------------------------------------- */
 

@@ -1251,6 +1251,53 @@ hrp_status hrp_brute_run(hrp_brute* b, int64_t n, const uint8_t* d_windows, int6
   return HRP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// One thread per (window, action): CoRun, Solo and each member's slot time (member i = window
+// position g_i, ascending; -1 padded).
+__global__ void job_times_kernel(DevSpace sp, DevPool pool, int64_t n,
+                                 const uint8_t* __restrict__ win, const int64_t* __restrict__ act,
+                                 int64_t* __restrict__ corun, int64_t* __restrict__ solo,
+                                 int64_t* __restrict__ mt) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = act[r];
+    int64_t* o = mt + r * 4;
+    if (a < 0 || a >= sp.n_actions) {
+      corun[r] = -1;
+      solo[r] = -1;
+      for (int i = 0; i < 4; ++i) o[i] = -1;
+      continue;
+    }
+    int g[4], sg[4], jobs[4];
+    int64_t st[4], so;
+    const int l = decode_action(sp, a, g, sg);
+    const int C = sp.lay_n[l];
+    corun[r] = corun_time(sp, pool, win + r * sp.W, l, g, sg, so, jobs, st);
+    solo[r] = so;
+    for (int i = 0; i < 4; ++i) o[i] = i < C ? st[sg[i]] : -1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+hrp_status hrp_job_times(hrp_brute* b, int64_t n, const uint8_t* d_windows,
+                         const int64_t* d_actions, int64_t* d_corun, int64_t* d_solo,
+                         int64_t* d_member_time, void* cuda_stream) {
+  if (!b || !d_windows || !d_actions || !d_corun || !d_solo || !d_member_time)
+    return fail(HRP_EINVAL, "NULL argument");
+  if (n < 0) return fail(HRP_EINVAL, "n < 0");
+  if (n == 0) return HRP_OK;
+  CK(cudaSetDevice(b->device));
+  job_times_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0,
+                     (cudaStream_t)cuda_stream>>>(b->dt.sp, b->dt.pool, n, d_windows, d_actions,
+                                                  d_corun, d_solo, d_member_time);
+  CK(cudaGetLastError());
+  return HRP_OK;
+}
+
 hrp_status hrp_brute_destroy(hrp_brute* b) {
   delete b;
   return HRP_OK;

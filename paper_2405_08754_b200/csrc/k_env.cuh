@@ -144,10 +144,11 @@ __device__ inline int64_t n_valid(const DevSpace& sp, uint64_t sched) {
   return nv;
 }
 
-// a6: CoRun, Solo of action (l, g, sigma) on window w (R7, R8).  Returns CoRun; sets solo.
+// a6: CoRun, Solo of action (l, g, sigma) on window w (R7, R8).  Returns CoRun; sets solo;
+// slot_t (optional) receives each slot's own time t_k (the job's CoRunAppTime).
 __device__ inline int64_t corun_time(const DevSpace& sp, const DevPool& pool, const uint8_t* w,
                                      int l, const int* g, const int* sg, int64_t& solo,
-                                     int* jobs_on_slot) {
+                                     int* jobs_on_slot, int64_t* slot_t = nullptr) {
   const int C = sp.lay_n[l];
   int64_t D[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -172,6 +173,7 @@ __device__ inline int64_t corun_time(const DevSpace& sp, const DevPool& pool, co
     if (X < 1000 * b8) X = 1000 * b8;
     const int64_t mem = ceil_div64(Tp * X, 1000 * b8);
     const int64_t t = comp > mem ? comp : mem;
+    if (slot_t) slot_t[k] = t;
     cr = t > cr ? t : cr;
     solo += Tp;
   }

@@ -75,6 +75,7 @@ def lib():
             "hrp_brute_create": [P, P, S, P, P],
             "hrp_brute_run": [P, i64, P, P, P, P, P, P],
             "hrp_brute_destroy": [P],
+            "hrp_job_times": [P, i64, P, P, P, P, P, P],
             "hrp_layout_table": [P, i32, P, P, P, P, P, P],
             "hrp_decode_action": [P, i64, P, P, P],
             "hrp_get_weights": [P, P],
@@ -224,6 +225,11 @@ def hrp_brute_create(space, profiles, device, cuda_stream):
 def hrp_brute_run(plan, n, d_windows, d_best, d_solo, d_rgs, d_bact, cuda_stream):
     _check(lib().hrp_brute_run(plan, int(n), _ptr(d_windows), _ptr(d_best), _ptr(d_solo),
                                _ptr(d_rgs), _ptr(d_bact), C.c_void_p(cuda_stream)))
+
+
+def hrp_job_times(plan, n, d_windows, d_actions, d_corun, d_solo, d_member_time, cuda_stream):
+    _check(lib().hrp_job_times(plan, int(n), _ptr(d_windows), _ptr(d_actions), _ptr(d_corun),
+                               _ptr(d_solo), _ptr(d_member_time), C.c_void_p(cuda_stream)))
 
 
 def hrp_brute_destroy(plan):
