@@ -64,16 +64,16 @@ def check_near_ties(orc, stats):
 
 
 def make_pair(cfgk, E, B, argmax_mode=2, lam=0.0, W=None, replay=None, workers=None,
-              oracle_argmax=None, variant=None):
+              oracle_argmax=None, variant=None, cmax=None):
     """variant: SURVEY §8(f)4 options for both sides, e.g. {"optimizer": "adam",
     "loss": "huber", "huber_kappa": 10.0}."""
     variant = dict(variant or {})
     from paper_2405_08754_b200.session import Session
     cfg = synth.config(cfgk)
-    if W is not None:
-        cfg = cfg.with_(space=cfg.space.__class__(W, cfg.space.cmax, cfg.space.shares,
-                                                  cfg.space.mig, cfg.space.interference_q3,
-                                                  lam))
+    if W is not None or cmax is not None:
+        cfg = cfg.with_(space=cfg.space.__class__(W or cfg.space.window, cmax or cfg.space.cmax,
+                                                  cfg.space.shares, cfg.space.mig,
+                                                  cfg.space.interference_q3, lam))
     pool = synth.make_pool(cfg.pool)
     sc = cfg.space
     osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
@@ -96,13 +96,14 @@ def make_pair(cfgk, E, B, argmax_mode=2, lam=0.0, W=None, replay=None, workers=N
 
 def run_lockstep(cfgk, E, B, steps, argmax_mode=2, lam=0.0, W=None, seed_step=0,
                  check_weights_every=1, name=None, workers=None, oracle_argmax=None,
-                 resync=False, drift_min_steps=None, variant=None):
+                 resync=False, drift_min_steps=None, variant=None, cmax=None):
     """drift_min_steps: free-running drift probe -- instead of failing, stop at the first step
     whose float outputs leave the tolerance, record it, and assert it is >= drift_min_steps."""
     from paper_2405_08754_b200.session import streams_to_dev
     t_start = time.time()
     cfg, pool, osp, sess, orc = make_pair(cfgk, E, B, argmax_mode, lam, W, workers=workers,
-                                          oracle_argmax=oracle_argmax, variant=variant)
+                                          oracle_argmax=oracle_argmax, variant=variant,
+                                          cmax=cmax)
     Wn = osp.W
     win0 = synth.make_windows(pool, E, Wn, step=seed_step)
     sess.reset(win0)
