@@ -525,12 +525,15 @@ def tensor_peak(burst=True):
                             "(tf32 ratio) x 1/3 (3xTF32 MMAs per product)")
 
 
-def alu_peak_tops():
-    """INT32/FP32 lane-op peak (T lane-ops/s): the measured microbenchmark when committed, else
-    148 SMs x 128 lanes x sm_max_mhz."""
+def alu_peak_tops(kind="fp32"):
+    """FP32 (kind "fp32": the selection kernels' fp32 adds / compares) or INT32 (kind "int":
+    the brute force) lane-op peak in T lane-ops/s: the measured add microbenchmark when
+    committed, else 148 SMs x 128 lanes x sm_max_mhz."""
     own = _own_peaks()
-    if own.get("alu_tops"):
-        return own["alu_tops"], "measured IADD3 microbenchmark (profiles/measured_peaks_r2.json)"
+    key = "alu_int_tops" if kind == "int" else "alu_tops"
+    if own.get(key):
+        return own[key], (f"measured {'int32' if kind == 'int' else 'fp32'} add microbenchmark "
+                          "(hrp_diag_alu, profiles/measured_peaks_r2.json)")
     pk = _peaks()
     return (148 * 128 * float(pk.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12,
             "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS)")
@@ -715,7 +718,7 @@ def run_brute(args, cfg):
     slot_terms = sum(comb(W, c) * int(nc[c]) * factorial(c) * 2 * c for c in range(1, 5))
     sec = ms / 1e3
     value = n * args.steps / sec
-    alu_peak, alu_src = alu_peak_tops()
+    alu_peak, alu_src = alu_peak_tops("int")
     ach = slot_terms * n * args.steps / sec / 1e12
     res = {"metric": "brute-force optimum windows/s (BASELINE config 3)", "value": value,
            "unit": "windows/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -778,7 +781,9 @@ def run_infer(args, cfg):
     th = synth.init_weights(osp.dims(cfg.net))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):
-        sess = Session(ecfg, pool, init_weights=th, device=local, stream=stream, replay=chunk)
+        # explicit enumeration: every valid action of every state is scored (the Q-evals metric)
+        sess = Session(ecfg, pool, init_weights=th, device=local, stream=stream, replay=chunk,
+                       argmax_mode=1)
         wins = synth.make_windows(pool, n, sc.window, step=5, rank=rank)
         sched = synth.sched_states(n, sc.window, rank=rank)
         wd = torch.from_numpy(wins).to(dev)

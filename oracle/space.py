@@ -177,6 +177,32 @@ def enumerate_layouts(cmax: int, shares, mig: bool = True):
     return out
 
 
+def mig_partitions(cmax: int):
+    """The MIG partitions with at most cmax CIs -- the whole GPU (MIG off) and every maximal GI
+    config x CI packing (R3/R4) -- as tuples of CIs (compute sm800 at 100 %, memory b8, domain),
+    in canonical layout order (they are the layouts whose CIs each host one process)."""
+    return [tuple((s.sm800, s.b8, s.dom) for s in lay.slots)
+            for lay in enumerate_layouts(cmax, (), True)]
+
+
+def default_mps_layouts(partition, cmax: int):
+    """MIG+MPS Default under reading R27: the MIG partition is fixed; each CI hosts
+    k >= 0 of the job set's members under MPS's default mode, modelled as equal shares
+    (sm800 = the CI's compute // k); 1 <= sum k <= cmax; CIs may stay idle.  Layouts in
+    lexicographic order of the per-CI counts, slots in CI order."""
+    out = []
+    n = len(partition)
+    for ks in itertools.product(range(cmax + 1), repeat=n):
+        if not 1 <= sum(ks) <= cmax:
+            continue
+        slots = []
+        for (sm, b8, dom), k in zip(partition, ks):
+            if k:
+                slots += [Slot(sm // k, b8, dom)] * k
+        out.append(Layout(True, (), (), (), tuple(slots)))
+    return out
+
+
 @dataclass
 class Space:
     """The layout table plus slot types for one (W, Cmax, S, MIG) configuration."""

@@ -134,3 +134,29 @@ def time_sharing_schedules(space, windows):
             p *= W - i
         off += p
     return [[off + j for j in range(W)] for _ in windows]
+
+
+def mig_partitions(W, cmax):
+    """The MIG partitions with at most cmax CIs (the whole GPU and every maximal GI config x CI
+    packing), from libhrp's layout table of the space with no MPS splits (each CI one process at
+    100 %): tuples of (sm800, b8, domain) per CI."""
+    tab = hrp.hrp_layout_table(hrp.make_space(W, cmax, (), True))
+    return [tuple((int(x["sm800"]), int(x["b8"]), int(x["dom"]))
+                  for x in tab["slots"][l][:tab["nslots"][l]]) for l in range(tab["n_layouts"])]
+
+
+def default_mps_table(partition, cmax):
+    """MIG+MPS Default (R27): the partition fixed, k >= 0 job-set members per
+    CI under MPS's default mode as equal shares (sm800 = CI compute // k), 1 <= sum k <= cmax:
+    an explicit layout table for hrp_space.n_layouts."""
+    import itertools
+    out = []
+    for ks in itertools.product(range(cmax + 1), repeat=len(partition)):
+        if not 1 <= sum(ks) <= cmax:
+            continue
+        lay = []
+        for (sm, b8, dom), k in zip(partition, ks):
+            if k:
+                lay += [(sm // k, b8, dom)] * k
+        out.append(lay)
+    return out

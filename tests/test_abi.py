@@ -79,3 +79,19 @@ def test_explicit_layout_table_round_trip():
     t = hrp.hrp_layout_table(hrp.make_space(6, 2, (50,), layouts=lay))
     assert t["n_layouts"] == 3 and list(t["nslots"]) == [1, 2, 2]
     assert t["n_actions"] == 6 + 30 + 30
+
+
+def test_mig_partitions_and_default_mps_tables_equal_oracle():
+    # MIG+MPS Default (R27): libhrp's partitions (the layouts of the space with no MPS
+    # splits) and the product-side default-MPS tables equal the oracle's own enumeration
+    from paper_2405_08754_b200.schedule import default_mps_table, mig_partitions
+    parts = mig_partitions(12, 4)
+    ref = SP.mig_partitions(4)
+    assert parts == ref and len(parts) == 39
+    for p in parts:
+        tab = default_mps_table(p, 4)
+        oref = SP.default_mps_layouts(p, 4)
+        assert tab == [[(s.sm800, s.b8, s.dom) for s in l.slots] for l in oref]
+        assert all(1 <= len(l) <= 4 for l in tab)
+        t = hrp.hrp_layout_table(hrp.make_space(12, 4, S10, True, layouts=tab))
+        assert t["n_layouts"] == len(tab)

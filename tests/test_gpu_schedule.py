@@ -125,3 +125,23 @@ def test_greedy_rollout_equals_oracle_greedy():
     assert sch == ref
     assert orc.near_ties <= 1
     orc.close()
+
+
+@pytest.mark.parametrize("pi", [0, 7, 17, 38])
+def test_mig_mps_default_tables_brute_force(pi):
+    # MIG+MPS Default (R27): the exhaustive optimum over one partition's default-MPS
+    # table, bit-exact against the oracle's DP over the oracle's own table of that partition
+    from paper_2405_08754_b200.schedule import default_mps_table, mig_partitions
+    from paper_2405_08754_b200.session import bruteforce
+    from oracle import brute as BR
+    pool = synth.make_pool(27)
+    part = mig_partitions(12, 4)[pi]
+    table = default_mps_table(part, 4)
+    scfg = synth.SpaceCfg(12, 4, S10)
+    sp = SP.build_space(12, 4, S10, True, layouts=SP.default_mps_layouts(SP.mig_partitions(4)[pi], 4))
+    Q = synth.table_v_windows(pool)[:4]
+    best, solo, rgs, bact = bruteforce(scfg, pool, Q, layouts=table)
+    for i, w in enumerate(Q):
+        ref = BR.dp_opt(sp, [int(x) for x in w], pool)
+        assert best[i] == ref["cost"] and solo[i] == ref["solo"]
+        assert list(rgs[i]) == ref["rgs"] and list(bact[i]) == ref["block_action"]

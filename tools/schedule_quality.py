@@ -3,6 +3,8 @@ P:291-305, Fig. 12 Fairness P:307-313) on Q1-Q12 (Table V, W = 12, Cmax = 4, P:2
 
 * Time Sharing, MIG Only (C = 2), MPS Only (C <= 4), MIG+MPS (C <= 4): the exhaustive optimum
   of each method's search space (P:245-248) -- hrp_brute_run;
+* MIG+MPS Default (C <= 4): one MIG partition for all queues (the one with the best average
+  optimum throughput over Q1-Q12), MPS in its default mode modelled as equal shares (R27);
 * MIG+MPS w/ RL: the duelling double-DQN agent trained with libhrp on config 3's space
   (class-stratified random windows, R18) and run greedily (epsilon = 0) on Q1-Q12 --
   hrp_env_step;
@@ -100,6 +102,19 @@ def main():
         timing[key] = time.perf_counter() - t
         methods[name] = job_metrics(plan, pool, Q, sch)
         assert all(m["corun"] == b for m, b in zip(methods[name], best)), "optimum mismatch"
+    # MIG+MPS Default (R27): one MIG partition for all queues, chosen by the average
+    # throughput over Q1-Q12 of the exhaustive optimum under it with equal (default) MPS shares
+    from paper_2405_08754_b200.schedule import default_mps_table, mig_partitions
+    best_p, best_am, per_p = None, -1.0, []
+    for part in mig_partitions(12, 4):
+        table = default_mps_table(part, 4)
+        plan = make_plan(space_of(full, table), prof)
+        sch, best = optimum_schedules(plan, Q)
+        am = float(np.mean(np.asarray(pool.solo_ticks, np.int64)[Q].sum(1) / best))
+        per_p.append((part, am))
+        if am > best_am:
+            best_p, best_am, best_plan, best_sch = part, am, plan, sch
+    methods["MIG+MPS Default (C<=4)"] = job_metrics(best_plan, pool, Q, best_sch)
     t = time.time()
     w, log, cfg = train_policy(pool, args.steps, args.envs, args.lr)
     train_s = time.time() - t
@@ -125,7 +140,9 @@ def main():
             "train_envs": args.envs, "lr": args.lr, "train_seconds": round(train_s, 1),
             "optimizer": "adam + huber(10)", "rl_throughput_fraction_of_optimum": rl_vs_opt,
             "rl_fraction_of_optimum_am": float(np.mean(rl_vs_opt)),
-            "rl_job_sets": rl, "optimum_seconds_per_call_12_windows":
+            "rl_job_sets": rl, "mig_mps_default_partition": best_p,
+            "mig_mps_default_am_per_partition": [[list(p), a] for p, a in per_p],
+            "optimum_seconds_per_call_12_windows":
                 {k: round(v, 4) for k, v in timing.items()}, "train_log": log}
     print(txt)
     print(json.dumps({k: v for k, v in meta.items() if k != "train_log"}))
