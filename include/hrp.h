@@ -182,6 +182,8 @@ hrp_status hrp_bruteforce_optimum(const hrp_space *space, const hrp_profiles *pr
                                   int64_t *d_block_action, void *cuda_stream);
 
 /* The same search with the layout space's tables kept resident: hrp_brute_create validates
+ * (the space must contain the whole-GPU single-slot layout, so that every window has a feasible
+ * schedule: EINVAL otherwise)
  * and uploads them once (synchronous; errors as hrp_bruteforce_optimum), hrp_brute_run only
  * enqueues the search kernel on `cuda_stream` (asynchronous, no allocation, graph-capturable),
  * hrp_brute_destroy frees the tables (after the caller's work on them is complete).

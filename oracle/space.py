@@ -188,9 +188,11 @@ def mig_partitions(cmax: int):
 def default_mps_layouts(partition, cmax: int):
     """MIG+MPS Default under reading R27: the MIG partition is fixed; each CI hosts
     k >= 0 of the job set's members under MPS's default mode, modelled as equal shares
-    (sm800 = the CI's compute // k); 1 <= sum k <= cmax; CIs may stay idle.  Layouts in
+    (sm800 = the CI's compute // k); 1 <= sum k <= cmax; CIs may stay idle.  A job left alone
+    may also take the whole GPU (time sharing, P:245 -- as in the MIG-only baseline), so every
+    window has a feasible schedule: that layout comes first, then the partition's layouts in
     lexicographic order of the per-CI counts, slots in CI order."""
-    out = []
+    out = [Layout(False, (), (), ((100,),), (Slot(800, 8, 0),))]
     n = len(partition)
     for ks in itertools.product(range(cmax + 1), repeat=n):
         if not 1 <= sum(ks) <= cmax:

@@ -1184,6 +1184,14 @@ hrp_status hrp_brute_create(const hrp_space* space, const hrp_profiles* prof, in
     return fail(HRP_ENOMEM, e.what());
   }
   if (hs.W > kBruteMaxW) return fail(HRP_ERANGE, "brute force supports W <= 12");
+  {
+    // every window needs a feasible schedule: a job alone on the whole GPU (CoRun = Solo)
+    bool whole = false;
+    for (int l = 0; l < hs.L; ++l)
+      whole |= hs.nslots[l] == 1 && hs.slots[l][0].sm800 == 800 && hs.slots[l][0].b8 == 8;
+    if (!whole)
+      return fail(HRP_EINVAL, "brute force needs the whole-GPU single-slot layout (time sharing)");
+  }
   if (hs.L > 512) return fail(HRP_ERANGE, "brute force supports <= 512 layouts");
   if (hs.n_actions() >= (int64_t(1) << kBruteIdxBits)) return fail(HRP_ERANGE, "|A| >= 2^26");
   // distinct memory sizes of the layout slots (the per-window memory-term table has a column

@@ -148,9 +148,10 @@ def mig_partitions(W, cmax):
 def default_mps_table(partition, cmax):
     """MIG+MPS Default (R27): the partition fixed, k >= 0 job-set members per
     CI under MPS's default mode as equal shares (sm800 = CI compute // k), 1 <= sum k <= cmax:
-    an explicit layout table for hrp_space.n_layouts."""
+    an explicit layout table for hrp_space.n_layouts.  A job left alone may also take the whole
+    GPU (time sharing, as in the MIG-only baseline): that layout comes first."""
     import itertools
-    out = []
+    out = [[(800, 8, 0)]]
     for ks in itertools.product(range(cmax + 1), repeat=len(partition)):
         if not 1 <= sum(ks) <= cmax:
             continue
