@@ -98,6 +98,11 @@ typedef struct {
   float huber_kappa;        /* h = delta^2/2 if |delta| <= kappa else kappa(|delta| - kappa/2) */
   int32_t precision;        /* 0 fp32-accurate 3xTF32 GEMMs; 1 fast mode: one TF32 MMA per   */
                             /* product (inputs rounded to tf32), policy-level parity only     */
+  int32_t agent;            /* 0 joint agent (R1/R2: factorised duelling head over (l, g,     */
+                            /* sigma)); 1 sequential agent (flat duelling */
+                            /* head [v, a_l] with one advantage per partition setup, P:259's  */
+                            /* "A = 29"; the job set is the next C_l jobs in queue order on   */
+                            /* slots in order).  Actions keep the joint index.               */
 } hrp_train_cfg;
 
 /* ---- lifecycle ------------------------------------------------------------------------ */

@@ -117,7 +117,10 @@ _WORKER = {}
 
 
 def _worker_init(space, argmax):
-    if argmax == "pruned":
+    if getattr(space, "seq", False):
+        off = A.offsets(space)
+        _WORKER["fn"] = lambda Fv, FcL, FcJ, s: greedy_seq(space, Fv, FcL, s, off)
+    elif argmax == "pruned":
         off = A.offsets(space)
         _WORKER["fn"] = lambda Fv, FcL, FcJ, s: PR.greedy_pruned(space, Fv, FcL, FcJ, s, off)
     else:
@@ -145,7 +148,10 @@ class OracleDQN:
         self.argmax = argmax
         self.workers = workers
         self._procs = None
-        if greedy is None and argmax == "pruned":
+        if greedy is None and getattr(space, "seq", False):
+            off = A.offsets(space)
+            greedy = lambda Fv, FcL, FcJ, s: greedy_seq(space, Fv, FcL, s, off)
+        elif greedy is None and argmax == "pruned":
             off = A.offsets(space)
             greedy = lambda Fv, FcL, FcJ, s: PR.greedy_pruned(space, Fv, FcL, FcJ, s, off)
         self.custom_greedy = greedy is not None
@@ -237,6 +243,8 @@ class OracleDQN:
         l, g, sg = A.decode(self.sp, theirs, self.off)
         if A.group_mask(g) & sched:
             raise AssertionError(f"GPU chose invalid action {theirs}")
+        if getattr(self.sp, "seq", False) and theirs != seq_action(self.sp, l, sched, self.off):
+            raise AssertionError(f"GPU chose a non-sequential action {theirs}")
         qt = QN.q_fixed(Fv, FcL, FcJ, self.sp, l, g, sg)
         gap = (qmax - qt) / 4294967296.0
         rel = gap / max(1.0, abs(qmax / 4294967296.0))
@@ -281,7 +289,10 @@ class OracleDQN:
         for e in range(E):
             sched = int(self.sched[e])
             v, cL, cJ, Fv, FcL, FcJ = hf[e]
-            if int(u_explore[e]) < int(thr):
+            if int(u_explore[e]) < int(thr) and getattr(sp, "seq", False):
+                vl = seq_valid_layouts(sp, sched)        # uniform over the valid setups
+                a = seq_action(sp, vl[A.explore_k(int(u_action[e]), len(vl))], sched, self.off)
+            elif int(u_explore[e]) < int(thr):
                 nv = A.n_valid(sp, sched)
                 a = A.kth_valid(sp, sched, A.explore_k(int(u_action[e]), nv), self.off)
             else:
@@ -404,6 +415,35 @@ class OracleDQN:
 def q_fixed_idx_any(space, off, Fv, FcL, FcJ, idx):
     l, g, sg = A.decode(space, int(idx), off)
     return QN.q_fixed(Fv, FcL, FcJ, space, l, g, sg)
+
+
+# -- the sequential agent (reading R28) -------------------------------
+# The paper's agent has V = 1 and A = 29 outputs (Table VI): one advantage per partition
+# setup.  Reading: the job set is the next C unscheduled jobs of the window in queue order
+# (first-come), member i on slot i; the agent chooses the setup l (C_l <= U).  The joint
+# action index of that (l, g, identity) keeps the reward, transition and replay of the joint
+# agent unchanged.
+
+def seq_action(space, l, sched, off=None):
+    free = [j for j in range(space.W) if not (sched >> j) & 1]
+    C = space.layouts[l].C
+    return A.action_index(space, l, tuple(free[:C]), tuple(range(C)), off)
+
+
+def seq_valid_layouts(space, sched):
+    U = space.W - bin(sched).count("1")
+    return [l for l, lay in enumerate(space.layouts) if lay.C <= U]
+
+
+def greedy_seq(space, Fv, FcL, sched, off=None):
+    """argmax over the valid setups of Q^ = F(v) + F(cL[l]), ties to the lowest l (= the lowest
+    joint index).  Returns (idx, Q^max)."""
+    best, bl = None, -1
+    for l in seq_valid_layouts(space, sched):
+        q = Fv + FcL[l]
+        if best is None or q > best:
+            best, bl = q, l
+    return (seq_action(space, bl, sched, off) if bl >= 0 else -1), best
 
 
 def greedy_bruteforce(space, Fv, FcL, FcJ, sched):

@@ -78,8 +78,10 @@ def backward(theta, dims, acts, dz, masks=None):
 
 
 def split_head(z, space):
-    """z [H] -> v, aL [L], aJ [W][T]."""
+    """z [H] -> v, aL [L], aJ [W][T] (all zero for the sequential agent's flat head, R28)."""
     L, W, T = space.L, space.W, space.T
+    if getattr(space, "seq", False):
+        return z[0], z[1:1 + L], np.zeros((W, T))
     return z[0], z[1:1 + L], z[1 + L:1 + L + W * T].reshape(W, T)
 
 
@@ -117,6 +119,8 @@ def dq_dz(space, l, g, sigma) -> np.ndarray:
     d[0] = 1.0
     d[1:1 + L] = -1.0 / L
     d[1 + l] += 1.0
+    if getattr(space, "seq", False):
+        return d                                  # flat head: no job-advantage block
     dJ = np.zeros((W, T))
     st = space.slot_type[l]
     for i, gi in enumerate(g):

@@ -213,6 +213,7 @@ class Space:
     layouts: list
     types: list          # [(sm800, b8)] ascending
     slot_type: list      # per layout: tuple of type ids in slot order
+    seq: bool = False    # sequential agent (reading R28): flat head [v, aL]
 
     @property
     def L(self) -> int:
@@ -224,16 +225,18 @@ class Space:
 
     @property
     def H(self) -> int:
-        """Head width 1 + L + W*T (value, layout advantages, job-slot-type advantages)."""
-        return 1 + self.L + self.W * self.T
+        """Head width 1 + L + W*T (value, layout advantages, job-slot-type advantages); the
+        sequential agent's flat head has 1 + L (value, one advantage per partition setup)."""
+        return 1 + self.L + (0 if self.seq else self.W * self.T)
 
 
-def build_space(W: int, cmax: int, shares, mig: bool = True, layouts=None) -> Space:
+def build_space(W: int, cmax: int, shares, mig: bool = True, layouts=None,
+                seq: bool = False) -> Space:
     lay = layouts if layouts is not None else enumerate_layouts(cmax, shares, mig)
     types = sorted({(s.sm800, s.b8) for l in lay for s in l.slots})
     tid = {t: i for i, t in enumerate(types)}
     st = [tuple(tid[(s.sm800, s.b8)] for s in l.slots) for l in lay]
-    return Space(W, cmax, lay, types, st)
+    return Space(W, cmax, lay, types, st, seq)
 
 
 def parse_notation(text: str):

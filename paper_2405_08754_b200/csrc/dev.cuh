@@ -12,6 +12,7 @@ __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) &
 // Layout space on the device (passed by value; arrays live in global memory).
 struct DevSpace {
   int W, cmax, L, T, H, q3;
+  int seq;                     // sequential agent (R28): flat head [v, aL], FIFO job sets
   const uint8_t* lay_n;        // [L] slots per layout
   const uint32_t* lay_stype;   // [L] 4 x u8 slot type ids (slot order)
   const uint32_t* lay_slot;    // [L*4] sm800 | b8 << 16 | dom << 24

@@ -150,6 +150,7 @@ hrp_status upload_tables(const HostSpace& hs, const hrp_profiles* prof, bool com
   }
   DevSpace& d = out.sp;
   d.W = W; d.cmax = hs.cmax; d.L = L; d.T = T; d.H = hs.head_width(); d.q3 = hs.q3;
+  d.seq = hs.seq ? 1 : 0;
   d.n_actions = hs.n_actions();
   CK(upload(ar, (uint8_t**)&d.lay_n, n.data(), L, st));
   CK(upload(ar, (uint8_t**)&d.lay_ndom, ndom.data(), L, st));
@@ -511,7 +512,8 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     // stream), head weight / bias gradients by fp64 scatter-adds (side stream) -- k_head.cuh
     const int w = c->dims[nl - 1];
     HeadArgs h{};
-    h.B = B; h.w = w; h.H = H; h.L = c->hs.L; h.T = c->hs.T; h.W = c->hs.W;
+    // the sequential agent's flat head has no job-advantage block: no slot types in the head
+    h.B = B; h.w = w; h.H = H; h.L = c->hs.L; h.T = c->hs.seq ? 0 : c->hs.T; h.W = c->hs.W;
     h.hdesc = c->hdesc;
     h.Wh = c->theta + c->woff[nl - 1];
     h.bh = h.Wh + (int64_t)w * H;
@@ -723,6 +725,8 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   } catch (const std::exception& e) {
     return fail(HRP_ENOMEM, e.what());
   }
+  if (cfg->agent < 0 || cfg->agent > 1) return fail(HRP_EINVAL, "agent must be 0 or 1");
+  c->hs.seq = cfg->agent == 1;
   const HostSpace& hs = c->hs;
   if (hs.L > 4096) return fail(HRP_ERANGE, "more than 4096 layouts");
   c->device = device;
@@ -739,7 +743,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   if (cfg->argmax_mode == 1 && hs.T > kXS) return fail(HRP_ERANGE, "explicit argmax needs <= 128 slot types");
   // auto = the exact pruned search (same actions bit for bit, faster at every measured config:
   // cfg 2 0.394 vs 0.424 ms/step, profiles/r1zo_bench_cfg2*.json)
-  c->explicit_mode = cfg->argmax_mode == 1;
+  c->explicit_mode = cfg->argmax_mode == 1 && !hs.seq;   // the flat head has its own argmax
   if ((s = upload_tables(hs, prof, false, c->ar, c->stream, c->dt))) return s;
   // network dims and flat parameter layout (W [out][in] then b [out] per layer)
   c->dims.push_back(hs.W * kRowIn);
@@ -1027,8 +1031,9 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   auto head_means = [&](const float* th, float* c0, float* mT) {
     const float* Wh = th + c->woff[nl - 1];
     prof_begin(c);
-    head_means_kernel<<<dim3(c->hs.T + 1, (hw + 1 + 31) / 32), 256, 0, c->stream>>>(
-        Wh, Wh + (int64_t)hw * H, hw, c->hs.L, c->hs.T, c->hs.W, c0, mT);
+    const int hT = c->hs.seq ? 0 : c->hs.T;
+    head_means_kernel<<<dim3(hT + 1, (hw + 1 + 31) / 32), 256, 0, c->stream>>>(
+        Wh, Wh + (int64_t)hw * H, hw, c->hs.L, hT, c->hs.W, c0, mT);
     return launch_check(c, HRP_K_HEAD_BWD);
   };
   auto target_pass = [&]() -> hrp_status {

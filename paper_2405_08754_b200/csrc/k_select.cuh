@@ -148,6 +148,10 @@ __device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict_
   float a = 0.f;
   for (int l = lane; l < sp.L; l += 32) a += z[1 + l];
   const float meanL = warp_sum(a) / (float)sp.L;
+  if (sp.seq) {          // the sequential agent's flat head has no job-advantage block
+    __syncwarp();
+    return meanL;
+  }
   const float* aJ = z + 1 + sp.L;
   for (int t = lane; t < sp.T; t += 32) {
     // four interleaved partial sums (independent load / add chains), combined in fixed order
@@ -630,11 +634,71 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   warp_best(best, bidx);
 }
 
+// ---------------------------------------------------------------------------------------
+// Sequential agent (reading R28): action = setup l with C_l <= U; the job set is
+// the next C_l unscheduled window positions in order, member i on slot i.  Joint index
+// off[l] + rank_lex(g) C! (identity permutation: Lehmer rank 0).
+
+__device__ inline int64_t seq_index(const DevSpace& sp, const PTabs& tb, int l, uint64_t sched) {
+  const int W = sp.W;
+  const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
+  uint64_t fm = all & ~sched;
+  const int C = tb.nsl[l];
+  int g[4];
+  for (int i = 0; i < C; ++i) {
+    g[i] = __ffsll((long long)fm) - 1;
+    fm &= fm - 1;
+  }
+  return tb.off[l] + rank_comb(g, C, W) * c_fact[C];
+}
+
+// Greedy: argmax over valid setups of F(v) + F(aL[l] - meanL), ties to the lowest l (= the
+// lowest joint index).  Lanes over layouts; result in all lanes; INT64_MAX if none is valid.
+__device__ inline void seq_greedy(const DevSpace& sp, const PTabs& tb, const float* __restrict__ z,
+                                  float meanL, uint64_t sched, int64_t& best, int64_t& bidx,
+                                  int64_t& nevals) {
+  const int lane = threadIdx.x & 31;
+  const int U = sp.W - __popcll(sched);
+  const int64_t Fv = fixed_point(z[0]);
+  best = INT64_MIN;
+  int64_t bl = INT64_MAX;
+  for (int l = lane; l < sp.L; l += 32) {
+    if (tb.nsl[l] > U) continue;
+    ++nevals;
+    const int64_t q = Fv + fixed_point(z[1 + l] - meanL);
+    if (q > best) { best = q; bl = l; }          // ascending l per lane: strict > keeps the lowest
+  }
+  warp_best(best, bl);
+  bidx = bl == INT64_MAX ? INT64_MAX : seq_index(sp, tb, (int)bl, sched);
+}
+
+// k-th valid setup (layout order) as its sequential action; lane-0 scan, result in all lanes.
+__device__ inline int64_t seq_kth(const DevSpace& sp, const PTabs& tb, uint64_t sched, int64_t k) {
+  const int U = sp.W - __popcll(sched);
+  int l = -1;
+  if ((threadIdx.x & 31) == 0) {
+    for (int i = 0; i < sp.L; ++i)
+      if (tb.nsl[i] <= U && k-- == 0) { l = i; break; }
+  }
+  l = __shfl_sync(0xffffffffu, l, 0);
+  return l < 0 ? -1 : seq_index(sp, tb, l, sched);
+}
+
+__device__ inline int64_t seq_n_valid(const DevSpace& sp, const PTabs& tb, uint64_t sched) {
+  const int U = sp.W - __popcll(sched);
+  int n = 0;
+  for (int l = threadIdx.x & 31; l < sp.L; l += 32) n += tb.nsl[l] <= U;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  return n;
+}
+
 template <int X>
 __device__ __forceinline__ void greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
                                        const float* __restrict__ z, float meanL, uint64_t sched,
                                        int64_t& best, int64_t& bidx, int64_t& nevals) {
-  if constexpr (X > 0) xgreedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+  if (sp.seq) seq_greedy(sp, tb, z, meanL, sched, best, bidx, nevals);
+  else if constexpr (X > 0) xgreedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
   else pwarp_greedy(sp, tb, w, z, meanL, sched, best, bidx, nevals);
 }
 
@@ -715,15 +779,15 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     }
     int64_t act = bidx;
     if ((uint64_t)a.u_explore[row] < a.thr) {
-      const int64_t nv = n_valid(sp, sched);
+      const int64_t nv = sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
       const int64_t k = (int64_t)__umul64hi(a.u_action[row], (uint64_t)nv);
-      act = pwarp_kth_valid(sp, tb, sched, k);
+      act = sp.seq ? seq_kth(sp, tb, sched, k) : pwarp_kth_valid(sp, tb, sched, k);
     } else if (bidx == INT64_MAX) {
       // a state always has a valid action, so no maximiser means non-finite Q values (NaN
       // weights): flag it for hrp_sync and keep the environment consistent with the lowest
       // valid action
       if (lane == 0) atomicOr(a.err, 1u);
-      act = pwarp_kth_valid(sp, tb, sched, 0);
+      act = sp.seq ? seq_kth(sp, tb, sched, 0) : pwarp_kth_valid(sp, tb, sched, 0);
     }
     const uint8_t* wr = a.win + (size_t)row * W;
     int64_t slot = 0;
@@ -754,7 +818,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
       uint64_t gm = 0;
       const uint32_t ty = tb.stype[l];
       for (int i = 0; i < C; ++i) {
-        q += Fj(sp, z, w.meanJ, g[i], (ty >> (8 * sg[i])) & 255);
+        if (!sp.seq) q += Fj(sp, z, w.meanJ, g[i], (ty >> (8 * sg[i])) & 255);
         gm |= 1ull << g[i];
       }
       const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
@@ -810,7 +874,7 @@ __device__ inline void write_desc(const DevSpace& sp, const PTabs& tb, int64_t i
   if (lane >= 1 && lane < 8) {
     int v;
     if (lane == 1) v = 1 + l;
-    else if (lane == 2) v = C;
+    else if (lane == 2) v = sp.seq ? 0 : C;     // job-advantage rows (none in the flat head)
     else if (lane < 7) v = lane - 3 < C ? 1 + sp.L + g[lane - 3] * sp.T + t[lane - 3] : -1;
     else v = (t[0] & 255) | (C > 1 ? (t[1] & 255) << 8 : 0) | (C > 2 ? (t[2] & 255) << 16 : 0) |
              (C > 3 ? (t[3] & 255) << 24 : 0);
@@ -864,7 +928,7 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
     const int* td = a.tdesc + (size_t)b * 8;
     int* hd = a.hdesc + (size_t)b * 8;
     float y = a.br[b];
-    if (td[2] > 0)
+    if (td[2] >= 0)   // -1: done (no bootstrap); 0 job rows in the flat head
       y += a.gamma * pwarp_qdesc(td, a.ht_hi + (size_t)b * a.w, a.ht_lo + (size_t)b * a.w, a.Wt,
                                  a.bt, a.c0t, a.mTt, a.w);
     const float q = pwarp_qdesc(hd, a.hs_hi + (size_t)b * a.w, a.hs_lo + (size_t)b * a.w, a.Wo,
@@ -918,7 +982,8 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
       if (astar == INT64_MAX) {   // non-finite Q (see sel_kernel): flag, lowest valid action
         if (lane == 0) atomicOr(a.err, 1u);
-        astar = pwarp_kth_valid(sp, tb, a.bsched[a.B + b], 0);
+        astar = sp.seq ? seq_kth(sp, tb, a.bsched[a.B + b], 0)
+                       : pwarp_kth_valid(sp, tb, a.bsched[a.B + b], 0);
       }
     }
     if (lane == 0 && a.astar) a.astar[b] = astar;

@@ -24,8 +24,9 @@ struct HostSpace {
   std::vector<std::array<uint8_t, 4>> stype;        // [L][4] type id per slot
   std::vector<std::pair<int, int>> types;           // [T] (sm800, b8) ascending
   std::vector<int64_t> off;                         // [L+1] action offsets
+  bool seq = false;                                 // sequential agent: flat head [v, aL]
   int64_t n_actions() const { return off.back(); }
-  int head_width() const { return 1 + L + W * T; }
+  int head_width() const { return 1 + L + (seq ? 0 : W * T); }
 };
 
 // Generate (or validate an explicit) layout table.  Returns HRP_OK or an error + message.

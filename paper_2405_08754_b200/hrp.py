@@ -48,7 +48,7 @@ class hrp_train_cfg(C.Structure):
                 ("lr", C.c_float), ("reward_lambda", C.c_float), ("argmax_mode", C.c_int32),
                 ("optimizer", C.c_int32), ("adam_beta1", C.c_float), ("adam_beta2", C.c_float),
                 ("adam_eps", C.c_float), ("loss", C.c_int32), ("huber_kappa", C.c_float),
-                ("precision", C.c_int32)]
+                ("precision", C.c_int32), ("agent", C.c_int32)]
 
 
 _lib = None
@@ -152,14 +152,16 @@ def make_profiles(pool):
 OPTIMIZERS = {"sgd": 0, "adam": 1}
 LOSSES = {"squared": 0, "huber": 1}
 PRECISIONS = {"3xtf32": 0, "fast": 1}
+AGENTS = {"joint": 0, "sequential": 1}
 
 
 def make_cfg(n_envs, batch, replay_capacity, hidden_layers, hidden_width, gamma=0.99, lr=1e-3,
              reward_lambda=0.0, argmax_mode=0, optimizer="sgd", adam=(0.9, 0.999, 1e-8),
-             loss="squared", huber_kappa=1.0, precision="3xtf32"):
+             loss="squared", huber_kappa=1.0, precision="3xtf32", agent="joint"):
     return hrp_train_cfg(n_envs, batch, replay_capacity, hidden_layers, hidden_width, gamma, lr,
                          reward_lambda, argmax_mode, OPTIMIZERS[optimizer], adam[0], adam[1],
-                         adam[2], LOSSES[loss], huber_kappa, PRECISIONS[precision])
+                         adam[2], LOSSES[loss], huber_kappa, PRECISIONS[precision],
+                         AGENTS[agent])
 
 
 # ---- entry points (same names as the C ABI) ---------------------------------------------

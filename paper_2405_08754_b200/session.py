@@ -18,7 +18,7 @@ class Session:
     def __init__(self, cfg, pool, n_envs=None, batch=None, init_weights=None, device=0,
                  rank=0, world=1, nccl_id=None, argmax_mode=0, replay=None,
                  reward_lambda=None, stream=None, optimizer="sgd", adam=(0.9, 0.999, 1e-8),
-                 loss="squared", huber_kappa=1.0, precision="3xtf32"):
+                 loss="squared", huber_kappa=1.0, precision="3xtf32", agent="joint"):
         if not torch.cuda.is_available():
             raise RuntimeError("libhrp needs a CUDA device (no CPU fallback)")
         self.cfg = cfg
@@ -33,7 +33,7 @@ class Session:
         self.tcfg = hrp.make_cfg(self.E, self.B, replay or max(1 << 16, 16 * self.E),
                                  cfg.net.hidden_layers, cfg.net.hidden_width, cfg.gamma, cfg.lr,
                                  lam, argmax_mode, optimizer, adam, loss, huber_kappa,
-                                 precision)
+                                 precision, agent)
         self.ctx = hrp.hrp_env_create(self.space, self.prof, self.tcfg, device,
                                       self.stream.cuda_stream, rank, world, nccl_id,
                                       init_weights)

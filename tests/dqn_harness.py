@@ -76,13 +76,15 @@ def make_pair(cfgk, E, B, argmax_mode=2, lam=0.0, W=None, replay=None, workers=N
                                                   cfg.space.interference_q3, lam))
     pool = synth.make_pool(cfg.pool)
     sc = cfg.space
-    osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
+    osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig,
+                         seq=variant.get("agent") == "sequential")
     dims = QN.net_dims(osp, cfg.net)
     theta0 = synth.init_weights(dims)
     N = replay or max(1 << 10, 4 * E)
     sess = Session(cfg, pool, n_envs=E, batch=B, init_weights=theta0, argmax_mode=argmax_mode,
                    replay=N, reward_lambda=lam, **variant)
     variant.pop("precision", None)
+    variant.pop("agent", None)
     assert sess.n_params == len(theta0)
     # the oracle's argmax: explicit enumeration where it is cheap, else the exact top-C search
     # (oracle/pruned.py, pinned against explicit enumeration); both give the same index

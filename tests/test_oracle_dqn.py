@@ -261,3 +261,37 @@ def test_adam_first_step_is_lr_times_sign():
     th1 = ag.theta.copy()
     ag.apply(g, False)
     np.testing.assert_allclose(ag.theta - th1, -0.01 * np.sign(g), atol=1e-9)
+
+
+def test_sequential_agent_hand_case_and_queue_order():
+    # SURVEY §8(f)2 / reading R28: flat head z = [v, a_0..a_{L-1}], the job set is the next C_l
+    # jobs in queue order.  W = 3, Cmax = 2, S = {50}, MIG off: layouts [(100)], [(50, 50)];
+    # v = 0, a = [1, 3] -> cL = [-1, 1]: from sched 0 the agent takes l = 1 on jobs (0, 1) --
+    # joint index off[1] + rank((0, 1)) * 2! + 0 = 3 + 0 = 3 -- then only l = 0 fits: job 2,
+    # index 2.
+    sp = SP.build_space(3, 2, (50,), False, seq=True)
+    assert sp.L == 2 and sp.H == 3
+    _, _, _, Fv, FcL, FcJ = EV.head_fixed(np.array([0.0, 1.0, 3.0]), sp)
+    assert EV.greedy_seq(sp, Fv, FcL, 0)[0] == 3
+    assert EV.greedy_seq(sp, Fv, FcL, 0b011)[0] == 2
+    # episodes take the jobs in queue order and schedule each exactly once
+    cfg = synth.config(1)
+    sp = SP.build_space(4, 2, (25, 50, 75), seq=True)
+    pool = synth.make_pool(27)
+    th = synth.init_weights(QN.net_dims(sp, cfg.net))
+    ag = EV.OracleDQN(sp, pool, cfg.net, th, 8, 8, 256)
+    ag.reset(synth.make_windows(pool, 8, 4))
+    order = [[] for _ in range(8)]
+    for t in range(8):
+        st = synth.step_streams(t, 8, 8, 4, pool)
+        a, r, d, cr, q = ag.env_step(synth.eps_threshold(t, 6), st["u_explore"], st["u_action"],
+                                     st["next_windows"])
+        for e in range(8):
+            l, g, s = A.decode(sp, int(a[e]))
+            assert s == tuple(range(len(g)))
+            order[e] += list(g)
+            if d[e]:
+                assert order[e] == [0, 1, 2, 3]
+                order[e] = []
+    out = ag.dqn_update(st["u_replay"], False)
+    assert np.isfinite(out["loss"]) and out["grad"].shape == th.shape

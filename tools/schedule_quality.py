@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 
-def train_policy(pool, steps, E, lr, seed_step=1000, log_every=250):
+def train_policy(pool, steps, E, lr, seed_step=1000, log_every=250, agent="joint"):
     """Train on config 3's space (W = 12, Cmax = 4, S = {10..90}) with a 3 x 256 Q-MLP, Adam +
     Huber (plain SGD on (1/2) delta^2 diverges at these reward scales), epsilon
     1 -> 0.01 over the first half.  Returns (online weights, training log)."""
@@ -37,11 +37,11 @@ def train_policy(pool, steps, E, lr, seed_step=1000, log_every=250):
     sc = synth.SpaceCfg(12, 4, tuple(range(10, 100, 10)))
     cfg = synth.config(2).with_(space=sc, n_decay=max(1, steps // 2), lr=lr, target_sync=100)
     tab = hrp.hrp_layout_table(space_of(sc))
-    H = 1 + tab["n_layouts"] + 12 * tab["n_types"]
+    H = 1 + tab["n_layouts"] + (12 * tab["n_types"] if agent == "joint" else 0)
     dims = [12 * 17] + [256] * 3 + [H]
     th = synth.init_weights(dims)
     sess = Session(cfg, pool, n_envs=E, batch=E, init_weights=th, replay=max(1 << 16, 16 * E),
-                   optimizer="adam", loss="huber", huber_kappa=10.0)
+                   optimizer="adam", loss="huber", huber_kappa=10.0, agent=agent)
     sess.reset(synth.make_windows(pool, E, 12, step=seed_step))
     log = []
     t0 = time.time()
@@ -59,13 +59,14 @@ def train_policy(pool, steps, E, lr, seed_step=1000, log_every=250):
             print(json.dumps(log[-1]), flush=True)
     w = sess.weights()[:sess.n_params].copy()
     sess.close()
-    return w, log, cfg
+    return w, log, cfg.with_(extra={"agent": agent})
 
 
 def rl_schedules(pool, Q, weights, cfg):
     from paper_2405_08754_b200.schedule import greedy_rollout
     from paper_2405_08754_b200.session import Session
-    sess = Session(cfg, pool, n_envs=len(Q), batch=len(Q), init_weights=weights, replay=1024)
+    sess = Session(cfg, pool, n_envs=len(Q), batch=len(Q), init_weights=weights, replay=1024,
+                   agent=cfg.extra.get("agent", "joint"))
     out = greedy_rollout(sess, Q)
     sess.close()
     return out
@@ -120,6 +121,11 @@ def main():
     train_s = time.time() - t
     rl = rl_schedules(pool, Q, w, cfg)
     methods["MIG+MPS w/ RL (C<=4)"] = job_metrics(full_plan, pool, Q, rl)
+    # the paper-literal sequential agent: flat head over the setups, job
+    # sets in queue order
+    ws, log_s, cfg_s = train_policy(pool, args.steps, args.envs, args.lr, agent="sequential")
+    rl_s = rl_schedules(pool, Q, ws, cfg_s)
+    methods["RL sequential (C<=4)"] = job_metrics(full_plan, pool, Q, rl_s)
     names = list(methods)
     lines = []
     for metric, key, fmt in (("Relative throughput (Solo / CoRun, Fig. 8)", "throughput", "{:.3f}"),
@@ -140,7 +146,8 @@ def main():
             "train_envs": args.envs, "lr": args.lr, "train_seconds": round(train_s, 1),
             "optimizer": "adam + huber(10)", "rl_throughput_fraction_of_optimum": rl_vs_opt,
             "rl_fraction_of_optimum_am": float(np.mean(rl_vs_opt)),
-            "rl_job_sets": rl, "mig_mps_default_partition": best_p,
+            "rl_job_sets": rl, "rl_sequential_job_sets": rl_s,
+            "mig_mps_default_partition": best_p,
             "mig_mps_default_am_per_partition": [[list(p), a] for p, a in per_p],
             "optimum_seconds_per_call_12_windows":
                 {k: round(v, 4) for k, v in timing.items()}, "train_log": log}
