@@ -24,6 +24,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# one JSON line on stdout: keep NCCL's banner off it (HRP_NCCL_DEBUG overrides)
+os.environ["NCCL_DEBUG"] = os.environ.get("HRP_NCCL_DEBUG", "WARN")
 
 import synth  # noqa: E402
 
@@ -267,6 +269,8 @@ def run_gpu(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     from paper_2405_08754_b200 import parallel
     nccl_id = parallel.nccl_unique_id(dev) if world > 1 else None
+    if world == 1 and args.comm1:
+        nccl_id = hrp.hrp_nccl_unique_id()    # one-rank communicator: the allreduce path on 1 GPU
     pool = synth.make_pool(cfg.pool)
     sc = cfg.space
     stream = torch.cuda.Stream(dev)
@@ -449,7 +453,9 @@ def run_gpu(args, cfg):
                           "l2": "flushed (256 MiB memset) between timed steps",
                           "launch": "CUDA graph per step (captured before the timed region)"
                                     if args.graph else "eager stream launches",
-                          "parallelism": f"dp{world} (env sharding + NCCL grad allreduce)"},
+                          "parallelism": f"dp{world} (env sharding + NCCL grad allreduce)"
+                                         + (" [one-rank NCCL communicator]" if world == 1 and
+                                            args.comm1 else "")},
                "q_evals_per_s": evals * world / (ms / 1e3),
                "q_evals_per_step": evals / args.steps,
                "q_evals_def": ("valid (state, joint action) pairs covered by the exact argmax of "
@@ -462,7 +468,8 @@ def run_gpu(args, cfg):
                        "d2h_bytes_per_step": int(d2h)},
                "clocks": clk,
                "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]}}
-        rl = rooflines(prof, args.steps, evals_k, cfg, osp, E, B, burst=at_max_clock(clk))
+        rl = rooflines(prof, args.steps, evals_k, cfg, osp, E, B, burst=at_max_clock(clk),
+                       explicit=sess_explicit(args, sc))
         res["roofline"] = dominant(rl, args.config)
         tot = sum(v["ms_per_step"] for v in rl.values())
         res["roofline"]["share_of_step"] = rl[res["roofline"]["kernel"]]["ms_per_step"] / tot
@@ -546,9 +553,11 @@ def _own_peaks():
         return {}
 
 
-def rooflines(prof, steps, evals, cfg, osp, E=None, B=None, burst=True):
+def rooflines(prof, steps, evals, cfg, osp, E=None, B=None, burst=True, explicit=True):
     """Per kernel class: achieved vs peak.  `evals` = (select, td)
-    explicit Q-evaluations over the timed steps; prof = {class: (ms, launches)}."""
+    explicit Q-evaluations over the timed steps; prof = {class: (ms, launches)}.  With the
+    pruned argmax (explicit False) the selection kernels' unit is the head output they read
+    once (E resp. B rows of H fp32 values): HBM-bound by construction."""
     pk = _peaks()
     alu_peak, alu_src = alu_peak_tops()
     fp32_tc, tc_src = tensor_peak(burst)
@@ -564,7 +573,14 @@ def rooflines(prof, steps, evals, cfg, osp, E=None, B=None, burst=True):
             continue
         sec = ms / 1e3
         per = {"ms_per_step": ms / steps, "launches_per_step": cnt / steps}
-        if name in ("select", "td"):
+        if name in ("select", "td") and not explicit:
+            rows = E if name == "select" else B
+            byts = rows * osp.H * 4
+            ach = byts * steps / sec / 1e9
+            per.update(bound="hbm", achieved=ach, peak=hbm, unit="GB/s", frac=ach / hbm,
+                       work=f"{byts / 1e6:.4g} MB/step (the head rows read once by the exact "
+                            "pruned argmax)")
+        elif name in ("select", "td"):
             n = evals[0] if name == "select" else evals[1]
             ach = 2.0 * n / sec / 1e12
             per.update(bound="alu", achieved=ach, peak=alu_peak, unit="Tops/s",
@@ -854,6 +870,9 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the timed steps eagerly instead of from per-step CUDA graphs")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--comm1", action="store_true",
+                    help="world 1 with a one-rank NCCL communicator: times the per-layer "
+                         "allreduce path (inside the per-step graphs) on one GPU")
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="weak: E per GPU fixed (default, configs 1-2); strong: the config's "
                          "global E and B sharded over the GPUs (default for config 4)")

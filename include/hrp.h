@@ -110,7 +110,8 @@ typedef struct {
 /* Create a context on `device` with CUDA stream `cuda_stream` (cudaStream_t or NULL).
  * rank/world: this process's place among `world` data-parallel replicas (one per GPU);
  * nccl_unique_id: 128-byte ncclUniqueId from hrp_nccl_unique_id() on rank 0, broadcast by the
- * caller (NULL iff world == 1).  init_weights: host fp32 [hrp_n_params] online weights
+ * caller (required for world > 1; with world == 1 a non-NULL id builds a one-rank NCCL
+ * communicator so that the allreduce path runs on one GPU -- a test configuration).  init_weights: host fp32 [hrp_n_params] online weights
  * (target := online), NULL = zeros.  Parameter layout: per Linear layer W [out][in]
  * row-major then b [out]; layer dims W*(f+5) -> w (x d) -> H = 1 + L + W*T (R1).
  * Errors: EINVAL, ERANGE (sizes), ENOMEM, ECUDA, ENCCL. */

@@ -484,7 +484,7 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out
 // complete -- on the side stream during the backward, so it overlaps the data-gradient chain of
 // the layers below.  Every rank issues the buckets in the same order (head first).
 hrp_status allreduce_layer(hrp_ctx* c, int i) {
-  if (c->world <= 1 || !c->allreduce) return HRP_OK;
+  if (c->comm == nullptr || !c->allreduce) return HRP_OK;
   const int nl = (int)c->dims.size() - 1;
   const int64_t o = c->woff[i];
   const int64_t n = (i + 1 < nl ? c->woff[i + 1] : c->n_params) - o;
@@ -905,7 +905,9 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->wsplitT, sizeof(float) * 2 * c->sstride));
   if ((s = split_weights(c.get(), false))) return s;
   if ((s = split_weights(c.get(), true))) return s;
-  if (world > 1) {
+  if (world > 1 || nccl_unique_id != nullptr) {
+    // world == 1 with an id: a one-rank communicator, so the allreduce path (per-layer buckets,
+    // side stream, graph capture) runs on a single GPU (tests)
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
     CKN(ncclCommInitRank(&c->comm, world, id, rank));
@@ -1003,7 +1005,7 @@ hrp_status hrp_q_forward(hrp_ctx* c, int64_t n, const uint8_t* d_windows, const 
 namespace {
 
 // a8-a12 of one double-DQN update: replay sample, forwards, TD argmax / loss, backward into
-// c->grad (allreduced per layer bucket when c->allreduce and world > 1).
+// c->grad (allreduced per layer bucket when c->allreduce and the context has a communicator).
 hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64_t* d_sample_idx,
                     int64_t* d_astar) {
   const int B = c->cfg.batch;

@@ -301,3 +301,46 @@ def test_cuda_graph_replay_equals_eager():
         for u, v in zip(x, y):
             assert torch.equal(u, v)
     assert torch.equal(outs[0][-1], outs[1][-1])
+
+
+def test_nccl_bucketed_allreduce_path_on_one_gpu():
+    # the per-layer allreduce buckets (side stream, NCCL calls captured in the
+    # per-step CUDA graphs) run on one GPU through a one-rank communicator; a sum over one rank
+    # is the identity, so the weights must equal the no-communicator context's bit for bit
+    from paper_2405_08754_b200 import hrp
+    from paper_2405_08754_b200.session import Session, streams_to_dev
+    cfg = synth.config(2)
+    pool = synth.make_pool(27)
+    osp = SP.build_space(16, 3, cfg.space.shares)
+    th = synth.init_weights(QN.net_dims(osp, cfg.net))
+    E = B = 256
+    outs = []
+    for nccl in (False, True):
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            sess = Session(cfg, pool, n_envs=E, batch=B, init_weights=th, replay=4096,
+                           stream=stream, nccl_id=hrp.hrp_nccl_unique_id() if nccl else None)
+            sess.reset(synth.make_windows(pool, E, 16))
+            steps = [streams_to_dev(synth.step_streams(t, E, B, 16, pool), sess.dev)
+                     for t in range(5)]
+            graphs = []
+            for t, d in enumerate(steps):
+                thr = synth.eps_threshold(t, cfg.n_decay)
+
+                def one(t=t, d=d, thr=thr):
+                    sess.step(thr, d["u_explore"], d["u_action"], d["next_windows"], extras=False)
+                    sess.update(d["u_replay"], t == 3, extras=False)
+                if t < 2:
+                    one()
+                    continue
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    one()
+                graphs.append(g)
+            for g in graphs:
+                g.replay()
+            stream.synchronize()
+            sess.sync()
+            outs.append(sess.weights())
+            sess.close()
+    assert np.array_equal(outs[0], outs[1])
