@@ -314,6 +314,7 @@ def run_gpu(args, cfg):
         ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         n_launch0 = sess.launches()
         evals0 = hrp.hrp_eval_counts(sess.ctx)
+        cov0 = hrp.hrp_covered_counts(sess.ctx)
         graphs = []
         if args.graph:
             # one CUDA graph per timed step (each step's inputs live at their own addresses and
@@ -346,6 +347,8 @@ def run_gpu(args, cfg):
         evals1 = hrp.hrp_eval_counts(sess.ctx)
         evals_k = (evals1[0] - evals0[0], evals1[1] - evals0[1])
         evals = evals_k[0] + evals_k[1]
+        cov1 = hrp.hrp_covered_counts(sess.ctx)
+        covered = (cov1[0] - cov0[0]) + (cov1[1] - cov0[1])
         ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
         # per-kernel breakdown: a separate pass over the same step inputs with per-launch CUDA
         # events on the context's stream (kept out of the timed region above: the extra
@@ -456,13 +459,16 @@ def run_gpu(args, cfg):
                           "parallelism": f"dp{world} (env sharding + NCCL grad allreduce)"
                                          + (" [one-rank NCCL communicator]" if world == 1 and
                                             args.comm1 else "")},
-               "q_evals_per_s": evals * world / (ms / 1e3),
-               "q_evals_per_step": evals / args.steps,
+               "q_evals_per_s": covered * world / (ms / 1e3),
+               "q_evals_per_step": covered / args.steps,
                "q_evals_def": ("valid (state, joint action) pairs covered by the exact argmax of "
-                               "a5 + a9: explicit mode counts every valid action (leaf rows "
-                               "whose exact fp32 suffix-max bound cannot beat the running "
-                               "maximum are not scored one by one); pruned mode counts the "
-                               "Top-list candidates scored"),
+                               "a5 + a9 (hrp_covered_counts): every valid action of every state "
+                               "whose greedy action was computed -- what an explicit "
+                               "enumeration scores; the exact search reaches the same maximum"),
+               "candidates_scored_per_s": evals * world / (ms / 1e3),
+               "candidates_def": ("actions actually scored (hrp_eval_counts): explicit mode, "
+                                  "the leaves not skipped by the fp32 suffix-max bound; pruned "
+                                  "mode, the Top-list assignments searched"),
                "gpu_launches": int(n_launch),
                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                        "d2h_bytes_per_step": int(d2h)},
@@ -810,13 +816,16 @@ def run_infer(args, cfg):
         def call():
             hrp.hrp_q_forward(sess.ctx, n, wd, sd, am, qm, None)
         e0 = hrp.hrp_eval_counts(sess.ctx)
+        c0 = hrp.hrp_covered_counts(sess.ctx)
         l0 = sess.launches()
         clocks = Clocks(local)
         ms = _timed_calls(call, args.steps, args.warmup, stream, flush)
         clk = clocks.stop()
         e1 = hrp.hrp_eval_counts(sess.ctx)
+        c1 = hrp.hrp_covered_counts(sess.ctx)
         launches = (sess.launches() - l0) / (args.steps + args.warmup)
-        evals = (e1[0] - e0[0]) / (args.steps + args.warmup)
+        scored = (e1[0] - e0[0]) / (args.steps + args.warmup)
+        evals = (c1[0] - c0[0]) / (args.steps + args.warmup)     # every valid action covered
         wh = torch.from_numpy(wins).pin_memory()
         sh = torch.from_numpy(sched.view(np.int64)).pin_memory()
         ah = torch.empty(n, dtype=torch.int64).pin_memory()
@@ -837,6 +846,7 @@ def run_infer(args, cfg):
         res = {"metric": "Q-evals/s (inference-only Q scoring, BASELINE config 5)",
                "value": evals * world * args.steps / sec, "unit": "Q-evals/s",
                "states_per_s": n * world * args.steps / sec,
+               "candidates_scored_per_s": scored * world * args.steps / sec,
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f32+i64", "data": "synthetic",

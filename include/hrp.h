@@ -264,6 +264,11 @@ int64_t hrp_eval_count(hrp_ctx *ctx);
 /* The same count split by kernel: out[0] = env step / inference selection, out[1] = the
  * double-DQN target argmax of hrp_dqn_update (host int64 [2]; synchronises the stream). */
 hrp_status hrp_eval_counts(hrp_ctx *ctx, int64_t *out);
+/* Valid actions covered by the exact argmax since create -- every valid (l, g, sigma) of each
+ * state whose greedy action was computed (the explicit enumeration's evaluations; the pruned
+ * search reaches the same maximum without scoring them one by one): out[0] env step /
+ * inference, out[1] the double-DQN target argmax (host int64 [2]; synchronises the stream). */
+hrp_status hrp_covered_counts(hrp_ctx *ctx, int64_t *out);
 /* Diagnostics: one tensor-core GEMM D[M][N] = A[M][K] . W[N][K]^T + bias (3xTF32, the Q-MLP
  * forward kernel) on `device` / `cuda_stream`, all pointers device; d_trace (optional,
  * uint64 [256]) receives %globaltimer stamps of CTA (0,0): [0] start, [1] setup, [2+kb] TMA

@@ -852,8 +852,9 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->br, R * 4));
   CK(ar.alloc((void**)&c->bdone, R));
   CK(ar.alloc((void**)&c->dsq, R * 4));
-  CK(ar.alloc((void**)&c->n_evals, 16));  // [0] select / inference kernels, [1] TD kernel
-  CK(cudaMemsetAsync(c->n_evals, 0, 16, c->stream));
+  // [0] select / inference candidates, [1] TD candidates, [2] / [3] valid actions covered
+  CK(ar.alloc((void**)&c->n_evals, 32));
+  CK(cudaMemsetAsync(c->n_evals, 0, 32, c->stream));
   CK(ar.alloc((void**)&c->sched_ctr, 4 * sizeof(unsigned)));   // select, TD, tdq ticket
   CK(cudaMemsetAsync(c->sched_ctr, 0, 4 * sizeof(unsigned), c->stream));
   CK(ar.alloc((void**)&c->dev_err, sizeof(unsigned)));
@@ -1385,6 +1386,17 @@ hrp_status hrp_get_hidden(hrp_ctx* c, int layer, int64_t rows, float* d_out) {
   const size_t w = (size_t)c->dims[layer + 1];
   CK(cudaMemcpyAsync(d_out, c->act[layer].hi, sizeof(float) * w * (size_t)rows,
                      cudaMemcpyDeviceToDevice, c->stream));
+  return HRP_OK;
+}
+
+hrp_status hrp_covered_counts(hrp_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(HRP_EINVAL, "NULL argument");
+  unsigned long long v[2] = {0, 0};
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(v, c->n_evals + 2, sizeof(v), cudaMemcpyDeviceToHost));
+  out[0] = (int64_t)v[0];
+  out[1] = (int64_t)v[1];
   return HRP_OK;
 }
 

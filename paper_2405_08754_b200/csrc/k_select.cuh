@@ -760,7 +760,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * pwarps(X > 0);
   const int W = sp.W;
-  int64_t nevals = 0;
+  int64_t nevals = 0, ncovered = 0;
   for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
     const float* zg = a.z + (size_t)row * sp.H;
     const float* z = zg;
@@ -768,6 +768,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     const float meanL = pwarp_means(sp, z, w.meanJ);
     int64_t best, bidx;
     greedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+    ncovered += sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
     if (a.mode == SEL_INFER) {
       if (lane == 0) {
         a.actions[row] = bidx == INT64_MAX ? -1 : bidx;
@@ -851,6 +852,8 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     int64_t tot = nevals;
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     if (lane == 0 && tot) atomicAdd(a.n_evals, (unsigned long long)tot);
+    // valid actions covered by the exact argmax (warp-uniform count), two counters on
+    if (lane == 0 && ncovered) atomicAdd(a.n_evals + 2, (unsigned long long)ncovered);
   }
 }
 
@@ -969,7 +972,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * pwarps(X > 0);
-  int64_t nevals = 0;
+  int64_t nevals = 0, ncovered = 0;
   for (int b = next_row(a.ctr, a.B, nw); b < a.B; b = next_row(a.ctr, a.B, nw)) {
     const bool done = a.bdone[b] != 0;
     int64_t astar = -1;
@@ -980,6 +983,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
       const float meanL = pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
+      ncovered += sp.seq ? seq_n_valid(sp, tb, a.bsched[a.B + b]) : n_valid(sp, a.bsched[a.B + b]);
       if (astar == INT64_MAX) {   // non-finite Q (see sel_kernel): flag, lowest valid action
         if (lane == 0) atomicOr(a.err, 1u);
         astar = sp.seq ? seq_kth(sp, tb, a.bsched[a.B + b], 0)
@@ -999,6 +1003,8 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
     int64_t tot = nevals;
     for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
     if (lane == 0 && tot) atomicAdd(a.n_evals, (unsigned long long)tot);
+    // valid actions covered by the exact argmax (warp-uniform count), two counters on
+    if (lane == 0 && ncovered) atomicAdd(a.n_evals + 2, (unsigned long long)ncovered);
   }
 }
 

@@ -86,6 +86,7 @@ def lib():
             "hrp_profile_read": [P, P, P],
             "hrp_eval_counts": [P, P],
             "hrp_diag_config": [S, S],
+            "hrp_covered_counts": [P, P],
             "hrp_diag_alu": [S, S, S, P],
             "hrp_diag_gemm": [S, P, S, S, S, P, P, P, P, P, S, S, P],
         }
@@ -338,6 +339,12 @@ def hrp_diag_gemm(device, cuda_stream, M, N, K, d_A, d_W, d_bias, d_D, reps=0, f
                                _ptr(d_A), _ptr(d_W), _ptr(d_bias), _ptr(d_D), None, int(reps),
                                int(force_bn), C.byref(ms)))
     return ms.value
+
+
+def hrp_covered_counts(ctx):
+    out = np.zeros(2, np.int64)
+    _check(lib().hrp_covered_counts(ctx, _hptr(out)))
+    return int(out[0]), int(out[1])
 
 
 def hrp_sync(ctx):

@@ -94,8 +94,14 @@ def test_q_forward_parity(cfgk, n, mode):
     wins, sched = _states(pool, n, osp.W, 5)
     dw = torch.from_numpy(wins).to(sess.dev)
     ds = torch.from_numpy(sched.view(np.int64)).to(sess.dev)
+    from paper_2405_08754_b200 import hrp
+    from oracle import actions as A
+    c0 = hrp.hrp_covered_counts(sess.ctx)
     am, qm, hd = sess.q_forward(dw, ds, head=True)
     torch.cuda.synchronize()
+    c1 = hrp.hrp_covered_counts(sess.ctx)
+    # the covered-actions counter is the number of valid actions of the scored states
+    assert c1[0] - c0[0] == sum(A.n_valid(osp, int(x)) for x in sched)
     a_o, q_o, z_o = orc.q_forward(wins, sched, gpu_argmax=am.cpu().numpy())
     np.testing.assert_array_equal(am.cpu().numpy(), a_o)
     close(qm.cpu().numpy(), q_o, what="qmax")
