@@ -25,6 +25,7 @@ using namespace hrp;
 // Instantiate F(X) for the selection-kernel variant v (0 pruned, 1..4 explicit, Cmax = v).
 #define HRP_VARIANT(v, F) \
   switch (v) {            \
+    case -1: F(-1); break; \
     case 0: F(0); break;  \
     case 1: F(1); break;  \
     case 2: F(2); break;  \
@@ -281,6 +282,9 @@ struct hrp_ctx {
   // dz, the head's two backward GEMMs become gathers / scatters
   int* hdesc = nullptr;               // [B][8]
   int* tdesc = nullptr;               // [B][8] (a* on s')
+  int64_t* bastar = nullptr;          // [B] a* when the caller passes none
+  int64_t *g_best = nullptr, *g_bidx = nullptr;   // [rows_max] sel_kernel -> sel_tail_kernel
+  float* g_meanL = nullptr;
   double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
   float *hc0 = nullptr, *hmT = nullptr;      // online head duelling-mean rows [w + 1], [T][w + 1]
   float *hc0t = nullptr, *hmTt = nullptr;    // target head
@@ -296,7 +300,8 @@ struct hrp_ctx {
   float *adam_m = nullptr, *adam_v = nullptr;   // Adam moments [n_params] (optimizer 1)
   int64_t adam_t = 0;                 // Adam updates applied
   size_t p_smem = 0;   // warp-per-state selection / TD kernels
-  int sel_variant = 0; // 0 pruned argmax, 1..4 explicit enumeration with Cmax = variant
+  int sel_variant = 0; // 0 / -1 pruned argmax (W <= 16 / W <= 64), 1..4 explicit enumeration
+                       // with Cmax = variant
   int p_grid = 0;
   int64_t launches = 0;
   TcGemm* tc = nullptr;
@@ -596,9 +601,17 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   prof_begin(c);
   const int rpc = sel_rows_per_cta(c->explicit_mode);
   const int grid = std::min((a.M + rpc - 1) / rpc, c->p_grid);
+  a.g_best = c->g_best;
+  a.g_bidx = c->g_bidx;
+  a.g_meanL = c->g_meanL;
 #define HRP_SEL(X) sel_kernel<X><<<grid, pwarps(X > 0) * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
   HRP_VARIANT(c->sel_variant, HRP_SEL);
 #undef HRP_SEL
+  hrp_status s = launch_check(c, HRP_K_SELECT);
+  if (s || a.mode != SEL_STEP) return s;
+  // a5-a7 per state: epsilon-greedy, reward, replay insert, transition, auto-reset
+  prof_begin(c);
+  sel_tail_kernel<<<(a.M + 7) / 8, 256, 0, c->stream>>>(c->dt.sp, c->dt.pool, a);
   return launch_check(c, HRP_K_SELECT);
 }
 
@@ -836,6 +849,10 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     const int T = hs.T;
     CK(ar.alloc((void**)&c->hdesc, sizeof(int) * 8 * (size_t)B));
     CK(ar.alloc((void**)&c->tdesc, sizeof(int) * 8 * (size_t)B));
+    CK(ar.alloc((void**)&c->bastar, sizeof(int64_t) * (size_t)B));
+    CK(ar.alloc((void**)&c->g_best, sizeof(int64_t) * (size_t)c->rows_max));
+    CK(ar.alloc((void**)&c->g_bidx, sizeof(int64_t) * (size_t)c->rows_max));
+    CK(ar.alloc((void**)&c->g_meanL, sizeof(float) * (size_t)c->rows_max));
     CK(ar.alloc((void**)&c->hacc, sizeof(double) * (size_t)H * (wd + 1)));
     CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)(T + 1) * (wd + 1)));
     CK(ar.alloc((void**)&c->hc0, sizeof(float) * (wd + 1)));
@@ -885,13 +902,13 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     CK(cudaFuncSetAttribute(sel_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, b)); \
     CK(cudaFuncSetAttribute(td_kernel<X>, cudaFuncAttributeMaxDynamicSharedMemorySize, b));  \
   } while (0)
-      HRP_ATTR(0); HRP_ATTR(1); HRP_ATTR(2); HRP_ATTR(3); HRP_ATTR(4);
+      HRP_ATTR(-1); HRP_ATTR(0); HRP_ATTR(1); HRP_ATTR(2); HRP_ATTR(3); HRP_ATTR(4);
 #undef HRP_ATTR
       p_smem_max[device & 63] = b;
     }
   }
   int occ = 1;
-  c->sel_variant = c->explicit_mode ? hs.cmax : 0;
+  c->sel_variant = c->explicit_mode ? hs.cmax : (hs.W > 16 ? -1 : 0);
   {
     cudaError_t e = cudaSuccess;
 #define HRP_OCC(X) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sel_kernel<X>, pwarps(X > 0) * 32, c->p_smem)
@@ -1081,7 +1098,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
     t.w = hw;
   }
   t.dsq = c->dsq;
-  t.astar = d_astar;
+  t.astar = d_astar ? d_astar : c->bastar;
   t.n_evals = c->n_evals + 1;
   t.ctr = c->sched_ctr + 1;
   t.err = c->dev_err;
@@ -1097,7 +1114,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   t.loss = d_loss;
   t.done_ctr = c->sched_ctr + 2;
   prof_begin(c);
-  tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(t);
+  tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(c->dt.sp, t);
   if ((s = launch_check(c, HRP_K_TD))) return s;
   return mlp_backward(c, B);
 }

@@ -215,6 +215,9 @@ struct SelArgs {
   unsigned long long* n_evals;  // optional evaluation counter
   unsigned* ctr;                // dynamic row scheduler (self-resetting, zero at create)
   unsigned* err;                // device error flag (bit 0: non-finite Q, see hrp_sync)
+  int64_t* g_best;              // [M] SEL_STEP: the greedy argmax per row (sel_kernel ->
+  int64_t* g_bidx;              //     sel_tail_kernel)
+  float* g_meanL;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -293,7 +296,7 @@ struct TdArgs {
   int* hdesc;           // structured head gradient: [B][8] per sample
                         //   {sc bits, 1 + l, C, rows 1 + L + g_i T + t_i (i < C; -1 pad) x 4,
                         //    t_0 | t_1 << 8 | t_2 << 16 | t_3 << 24}, sc = delta / (B world)
-  int64_t* astar;       // [B] optional
+  int64_t* astar;       // [B] a* (-1 when done): td_kernel -> tdq_kernel
   // sparse Q: Q(s, a) and Q_target(s', a*) from the last hidden activations and the
   // head rows they need, Q = h . (c0 + W[1 + l] + sum_i (W[r_i] - mT[t_i])) + (same on biases),
   // instead of full online-head rows for s and target-head rows for s'

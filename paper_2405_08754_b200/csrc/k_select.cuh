@@ -1,11 +1,15 @@
 // Warp-per-state selection kernels of libhrp (sm_100a):
-//   sel_kernel<X>  (X = 0: pruned argmax; X = 1..4: explicit enumeration with Cmax = X)
-//                  a4-a7 fused: duelling centering + fixed point (R15, R20), greedy
-//                  argmax, epsilon-greedy (R14), co-run reward (P:122, P:139-140,
-//                  Table VI, R7-R9), transition + replay insert + auto-reset
-//                  (R19); or inference (epsilon = 0)
-//   td_kernel<X>   a9-a10: double-DQN target argmax on s', target Q, TD error, loss
-//                  term, structured head gradient of (1/2) delta^2
+//   sel_kernel<X>  (X = 0 / -1: pruned argmax for W <= 16 / W <= 64; X = 1..4: explicit
+//                  enumeration with Cmax = X) a4-a5: duelling centering + fixed point (P:242,
+//                  R15, R20) and the greedy argmax per state; inference outputs directly
+//   sel_tail_kernel a5-a7: epsilon-greedy (R14), co-run reward (P:122, P:139-140,
+//                  Table VI, R7-R9), transition + replay insert + auto-reset (P:112-122,
+//                  R19), one warp per state
+//   td_kernel<X>   a9: double-DQN target argmax a* on s'
+//   tdq_kernel     a9-a10: action descriptors of a and a*, target Q, TD error, loss term,
+//                  structured head gradient of (1/2) delta^2
+// The argmax kernels carry only the argmax (their code must stay inside the instruction cache:
+// the per-state tails are separate kernels).
 // One warp owns one state at a time; no block-wide barriers.  The head row z is read from
 // global memory (L2-resident, coalesced across lanes).  Two exact greedy argmax algorithms:
 //
@@ -116,7 +120,8 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
     w.pos = (int*)wb;
   } else {
     w.top = (int*)wb;
-    w.topv = (int64_t*)(wb + align16(sizeof(int) * sp.T * 4));
+    wb += align16(sizeof(int) * sp.T * 4);
+    w.topv = (int64_t*)wb;
   }
   for (int i = threadIdx.x; i <= sp.L; i += blockDim.x) t.off[i] = sp.off[i];
   for (int i = threadIdx.x; i < sp.L; i += blockDim.x) {
@@ -165,6 +170,104 @@ __device__ inline float pwarp_means(const DevSpace& sp, const float* __restrict_
     }
     for (; j < sp.W; ++j) s0 += aJ[j * sp.T + t];
     meanJ[t] = ((s0 + s1) + (s2 + s3)) / (float)sp.W;
+  }
+  __syncwarp();
+  return meanL;
+}
+
+// F(x) as an integer-valued fp32: rint(x 2^32) is exact in fp32 and orders like F; values at or
+// above 2^63 are clamped to 2^63, which __float2ll_rn saturates to INT64_MAX as fixed_point does.
+__device__ __forceinline__ float f_as_float(float x) {
+  return fminf(rintf(x * 4294967296.0f), 9223372036854775808.0f);
+}
+
+// One lane, one slot type t (column col = aJ + t, stride T) of a head row, W <= 16 NJ: the
+// duelling mean meanJ[t] in pwarp_means' order (same bits) and the Top-4 list of t.  All W
+// values are loaded at once into registers (independent loads: their latency overlaps).
+// Threshold: the free positions are cut into 16 groups (position mod 16); the 4th largest of
+// the 16 group maxima m4 is attained by 4 distinct free positions and F(a - mean) is monotone in
+// a, so every Top-4 member has F >= F(m4 - mean).  The positions passing that filter form a
+// 64-bit candidate mask (no divergent work per position); the few candidates are then inserted
+// in ascending position order by (F desc, j asc) -- the Top-4 of the full scan, ties included
+// (with heavy ties the mask simply holds more positions).
+template <int NJ>
+__device__ __forceinline__ void ptop_type(const float* __restrict__ col, int T, int W,
+                                          uint64_t freem, int t, bool tv, PWarpSmem& w) {
+  constexpr int NU = 16 * NJ;
+  const float ninf = -INFINITY;
+  const int w4 = (W >> 2) << 2;
+  float x[NU];
+#pragma unroll
+  for (int u = 0; u < NU; ++u) x[u] = (tv && u < W) ? col[u * T] : 0.f;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {   // chunks of 4 into s0..s3, the W % 4 tail into s0 (ascending)
+    if (u < w4) s[u & 3] += x[u];
+    else if (u < W) s[0] += x[u];
+  }
+  const float mj = ((s[0] + s[1]) + (s[2] + s[3])) / (float)W;
+  float gm[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) gm[u] = ninf;
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+    if ((freem >> u) & 1) gm[u & 15] = fmaxf(gm[u & 15], x[u]);
+  float b0 = ninf, b1 = ninf, b2 = ninf, b3 = ninf;   // the 4 largest group maxima
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    float v = gm[u], h;
+    h = fmaxf(b0, v); v = fminf(b0, v); b0 = h;
+    h = fmaxf(b1, v); v = fminf(b1, v); b1 = h;
+    h = fmaxf(b2, v); v = fminf(b2, v); b2 = h;
+    b3 = fmaxf(b3, v);
+  }
+  const float thr = b3 == ninf ? ninf : f_as_float(b3 - mj);
+  uint64_t cm = 0;
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+    if (f_as_float(x[u] - mj) >= thr) cm |= 1ull << u;
+  cm &= freem;
+  if (!tv) return;
+  w.meanJ[t] = mj;
+  // (F desc, j asc): candidates in ascending j, strict > keeps the lower position; F = INT64_MIN
+  // (x 2^32 <= -2^63) is never a Top entry, as in ptop_scan_one
+  float v0 = -9223372036854775808.0f, v1 = v0, v2 = v0, v3 = v0;
+  int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
+  for (; cm; cm &= cm - 1) {
+    const int jc = __ffsll((long long)cm) - 1;
+    const float y = f_as_float(col[jc * T] - mj);
+    if (!(y > v3)) continue;
+    v3 = y; j3 = jc;
+    if (v3 > v2) { float u = v2; v2 = v3; v3 = u; int q = j2; j2 = j3; j3 = q; }
+    if (v2 > v1) { float u = v1; v1 = v2; v2 = u; int q = j1; j1 = j2; j2 = q; }
+    if (v1 > v0) { float u = v0; v0 = v1; v1 = u; int q = j0; j0 = j1; j1 = q; }
+  }
+  w.top[t * 4 + 0] = j0; w.top[t * 4 + 1] = j1; w.top[t * 4 + 2] = j2; w.top[t * 4 + 3] = j3;
+  w.topv[t * 4 + 0] = j0 < 0 ? INT64_MIN : __float2ll_rn(v0);
+  w.topv[t * 4 + 1] = j1 < 0 ? INT64_MIN : __float2ll_rn(v1);
+  w.topv[t * 4 + 2] = j2 < 0 ? INT64_MIN : __float2ll_rn(v2);
+  w.topv[t * 4 + 3] = j3 < 0 ? INT64_MIN : __float2ll_rn(v3);
+}
+
+// Pruned mode (X = 0: W <= 16, NJ = 1; X = -1: W <= 64, NJ = 4): meanL and, lane <-> slot type,
+// meanJ and the Top-4 lists of every slot type from one read of the head row
+// (ptop_type).  Returns meanL.
+template <int NJ>
+__device__ inline float pwarp_means_top(const DevSpace& sp, const float* __restrict__ z,
+                                        uint64_t sched, PWarpSmem& w) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();  // previous readers of meanJ / Top lists are done
+  float a = 0.f;
+  for (int l = lane; l < sp.L; l += 32) a += z[1 + l];
+  const float meanL = warp_sum(a) / (float)sp.L;
+  const int W = sp.W, T = sp.T;
+  const float* aJ = z + 1 + sp.L;
+  const uint64_t freem = (W == 64 ? ~0ull : ((1ull << W) - 1)) & ~sched;
+  for (int t0 = 0; t0 < T; t0 += 32) {      // warp-uniform passes of 32 slot types
+    const int t = t0 + lane;
+    const bool tv = t < T;
+    const float* col = aJ + (tv ? t : 0);
+    ptop_type<NJ>(col, T, W, freem, t, tv, w);
   }
   __syncwarp();
   return meanL;
@@ -550,45 +653,24 @@ __device__ __forceinline__ void psearch(const PTabs& tb, const PWarpSmem& w, int
   }
 }
 
-// Greedy (exact pruned) argmax of one state by one warp.  Returns (best, bidx) in all lanes;
-// bidx = INT64_MAX when no action is valid.
+// Greedy (exact pruned) argmax of one state by one warp over the Top lists pwarp_means_top
+// built.  Returns (best, bidx) in all lanes; bidx = INT64_MAX when no action is valid.
 __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
                                     const float* __restrict__ z, float meanL, uint64_t sched,
                                     int64_t& best, int64_t& bidx, int64_t& nevals) {
   const int lane = threadIdx.x & 31;
-  const int W = sp.W, T = sp.T;
-  const float* aJ = z + 1 + sp.L;
-  const uint64_t freem = (W == 64 ? ~0ull : ((1ull << W) - 1)) & ~sched;
-  for (int t = lane; t < T; t += 32) {
-    // top-4 by (value desc, position asc): register-only insertion network.  x < x3 (fp32)
-    // implies F(x) <= F(x3) = b3 (F is monotone), so most positions are rejected before the
-    // fixed-point conversion; the exact test is still on F.
-    int64_t b0 = INT64_MIN, b1 = INT64_MIN, b2 = INT64_MIN, b3 = INT64_MIN;
-    float x0 = -INFINITY, x1 = -INFINITY, x2 = -INFINITY, x3 = -INFINITY;
-    int j0 = -1, j1 = -1, j2 = -1, j3 = -1;
-    const float mj = w.meanJ[t];
-    for (uint64_t fm = freem; fm; fm &= fm - 1) {   // free positions, ascending (warp-uniform)
-      const int j = __ffsll((long long)fm) - 1;
-      const float x = aJ[j * T + t] - mj;
-      if (x < x3) continue;
-      const int64_t v = fixed_point(x);
-      if (v <= b3) continue;  // ties keep the lower position
-      b3 = v; j3 = j; x3 = x;
-      if (b3 > b2) { int64_t u = b2; b2 = b3; b3 = u; int y = j2; j2 = j3; j3 = y; float f = x2; x2 = x3; x3 = f; }
-      if (b2 > b1) { int64_t u = b1; b1 = b2; b2 = u; int y = j1; j1 = j2; j2 = y; float f = x1; x1 = x2; x2 = f; }
-      if (b1 > b0) { int64_t u = b0; b0 = b1; b1 = u; int y = j0; j0 = j1; j1 = y; float f = x0; x0 = x1; x1 = f; }
-    }
-    (void)x0;
-    w.top[t * 4 + 0] = j0; w.top[t * 4 + 1] = j1; w.top[t * 4 + 2] = j2; w.top[t * 4 + 3] = j3;
-    w.topv[t * 4 + 0] = b0; w.topv[t * 4 + 1] = b1; w.topv[t * 4 + 2] = b2; w.topv[t * 4 + 3] = b3;
-  }
-  __syncwarp();
+  const int W = sp.W;
+  (void)sched;
+  __syncwarp();   // Top lists written by pwarp_means_top
   const int64_t Fv = fixed_point(z[0]);
   best = INT64_MIN;
   bidx = INT64_MAX;
   // Seed: per layout the first leaf of its search (slot k takes its best Top-list job not
   // already taken) -- a valid action, so (best, bidx) may start at the warp's best seed; the
   // bound then prunes most layouts at the first level.
+  int64_t sv = INT64_MIN;
+  int sl = INT32_MAX;
+  int sjs[4] = {0, 0, 0, 0};
   for (int i = lane; i < sp.L; i += 32) {
     const int l = tb.lay_of_c[i];
     const int C = tb.nsl[l];
@@ -611,11 +693,20 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
         if (!used) { js[k] = j; v += w.topv[t * 4 + q]; ok = true; break; }
       }
     }
-    if (!ok || v < best) continue;
-    if (C == 1) pleaf<1>(tb, l, W, js, v, best, bidx);
-    else if (C == 2) pleaf<2>(tb, l, W, js, v, best, bidx);
-    else if (C == 3) pleaf<3>(tb, l, W, js, v, best, bidx);
-    else pleaf<4>(tb, l, W, js, v, best, bidx);
+    // the lane's best seed by (value desc, layout asc) = (value desc, action index asc): only
+    // that one is ranked
+    if (!ok || v < sv || (v == sv && l > sl)) continue;
+    sv = v;
+    sl = l;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sjs[k] = js[k];
+  }
+  if (sl < sp.L) {
+    const int C = tb.nsl[sl];
+    if (C == 1) pleaf<1>(tb, sl, W, sjs, sv, best, bidx);
+    else if (C == 2) pleaf<2>(tb, sl, W, sjs, sv, best, bidx);
+    else if (C == 3) pleaf<3>(tb, sl, W, sjs, sv, best, bidx);
+    else pleaf<4>(tb, sl, W, sjs, sv, best, bidx);
   }
   warp_best(best, bidx);
   // Exhaustive pruned search, lanes over layouts grouped by slot count (C-uniform rounds).
@@ -751,101 +842,135 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
   return -1;
 }
 
+// a5-a7 after the greedy argmax (best, bidx) of row `row` (one warp; z = its head row, tables in
+// global memory): epsilon-greedy choice (R14), co-run reward (R7-R9), replay insert, transition
+// and auto-reset (R19).
+__device__ inline void sel_tail(const DevSpace& sp, const DevPool& pool, const PTabs& tb,
+                                const SelArgs& a, int row, const float* z, float meanL,
+                                uint64_t sched, int64_t best, int64_t bidx) {
+  const int lane = threadIdx.x & 31;
+  const int W = sp.W;
+  int64_t act = bidx;
+  if ((uint64_t)a.u_explore[row] < a.thr) {
+    const int64_t nv = sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
+    const int64_t k = (int64_t)__umul64hi(a.u_action[row], (uint64_t)nv);
+    act = sp.seq ? seq_kth(sp, tb, sched, k) : pwarp_kth_valid(sp, tb, sched, k);
+  } else if (bidx == INT64_MAX) {
+    // a state always has a valid action, so no maximiser means non-finite Q values (NaN
+    // weights): flag it for hrp_sync and keep the environment consistent with the lowest
+    // valid action
+    if (lane == 0) atomicOr(a.err, 1u);
+    act = sp.seq ? seq_kth(sp, tb, sched, 0) : pwarp_kth_valid(sp, tb, sched, 0);
+  }
+  const uint8_t* wr = a.win + (size_t)row * W;
+  int64_t slot = 0;
+  int d = 0;
+  int g[4], sg[4];
+  const int l = decode_action(sp, act, g, sg);   // every lane (same result)
+  const int C = tb.nsl[l];
+  const uint32_t ty = tb.stype[l];
+  // slot-type means of the action's members, summed from the head row in pwarp_means' order
+  // (same bits): lane 4i + q sums s_q of member i's type
+  float mjv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (!sp.seq) {
+    const int i = lane >> 2, q = lane & 3;
+    const int T = sp.T, w4 = (W >> 2) << 2;
+    float sq = 0.f;
+    if (i < C) {
+      const float* aJ = z + 1 + sp.L + ((ty >> (8 * sg[i])) & 255);
+      for (int j = q; j < w4; j += 4) sq += aJ[j * T];
+      if (q == 0)
+        for (int j = w4; j < W; ++j) sq += aJ[j * T];
+    }
+    const float s1 = __shfl_down_sync(0xffffffffu, sq, 1);
+    const float s2 = __shfl_down_sync(0xffffffffu, sq, 2);
+    const float s3 = __shfl_down_sync(0xffffffffu, sq, 3);
+    const float mj = ((sq + s1) + (s2 + s3)) / (float)W;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mjv[k] = __shfl_sync(0xffffffffu, mj, 4 * k);
+  }
+  if (lane == 0) {
+    int jobs[4];
+    int64_t solo;
+    const int64_t cr = corun_time(sp, pool, wr, l, g, sg, solo, jobs);
+    double r = ((double)solo / (double)cr - 1.0) * 100.0;
+    if (a.lam != 0.f) {
+      int64_t sc = 0, sm = 0, sT = 0;
+      for (int j = 0; j < W; ++j) { sc += pool.c[wr[j]]; sm += pool.m[wr[j]]; sT += pool.T[wr[j]]; }
+      const double cb = (double)sc / W, mb = (double)sm / W, Tb = (double)sT / W;
+      double ri = 0.0;
+      for (int k = 0; k < C; ++k) {
+        const uint32_t sl = sp.lay_slot[l * 4 + k];
+        const int p = jobs[k];
+        const double dr = (double)pool.T[p] / Tb;
+        ri += ((double)(sl & 0xffff) / 800.0 * ((double)pool.c[p] / cb) +
+               (double)((sl >> 16) & 255) / 8.0 * ((double)pool.m[p] / mb)) * dr * dr;
+      }
+      r += (double)a.lam * ri;
+    }
+    int64_t q = fixed_point(z[0]) + fixed_point(z[1 + l] - meanL);
+    uint64_t gm = 0;
+    for (int i = 0; i < C; ++i) {
+      if (!sp.seq)
+        q += fixed_point(z[1 + sp.L + g[i] * sp.T + ((ty >> (8 * sg[i])) & 255)] - mjv[i]);
+      gm |= 1ull << g[i];
+    }
+    const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
+    const uint64_t s2 = sched | gm;
+    d = s2 == all;
+    slot = (a.t_step * (int64_t)a.M + row) % a.N_rep;
+    a.rep_sched[2 * slot] = sched;       // s
+    a.rep_sched[2 * slot + 1] = s2;      // s' (the action's jobs scheduled)
+    a.rep_act[slot] = act;
+    a.rep_r[slot] = (float)r;
+    a.rep_done[slot] = (uint8_t)d;
+    a.actions[row] = act;
+    a.rewards[row] = (float)r;
+    a.done[row] = (uint8_t)d;
+    if (a.corun) a.corun[row] = cr;
+    if (a.qsel) a.qsel[row] = (float)((double)q * (1.0 / 4294967296.0));
+    if (a.greedy) a.greedy[row] = bidx == INT64_MAX ? -1 : bidx;
+    a.sched[row] = d ? 0ull : s2;
+  }
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  d = __shfl_sync(0xffffffffu, d, 0);
+  uint8_t* wm = a.win + (size_t)row * W;
+  for (int j = lane; j < W; j += 32) a.rep_win[slot * W + j] = wm[j];
+  __syncwarp();
+  if (d)
+    for (int j = lane; j < W; j += 32) wm[j] = a.next_win[(size_t)row * W + j];
+  __syncwarp();
+}
+
 template <int X>
-__global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 : 4))
+__global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 : 4))
 sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * pwarps(X > 0);
-  const int W = sp.W;
   int64_t nevals = 0, ncovered = 0;
   for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
     const float* zg = a.z + (size_t)row * sp.H;
     const float* z = zg;
     const uint64_t sched = a.sched[row];
-    const float meanL = pwarp_means(sp, z, w.meanJ);
+    const float meanL = (X <= 0 && !sp.seq) ? pwarp_means_top<X == 0 ? 1 : 4>(sp, z, sched, w)
+                                            : pwarp_means(sp, z, w.meanJ);
     int64_t best, bidx;
     greedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
     ncovered += sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
-    if (a.mode == SEL_INFER) {
-      if (lane == 0) {
+    if (lane == 0) {
+      if (a.mode == SEL_INFER) {
         a.actions[row] = bidx == INT64_MAX ? -1 : bidx;
         a.qmax[row] = bidx == INT64_MAX ? __int_as_float(0x7fc00000)
                                         : (float)((double)best * (1.0 / 4294967296.0));
+      } else {   // the rest of a5-a7: sel_tail_kernel
+        a.g_best[row] = best;
+        a.g_bidx[row] = bidx;
+        a.g_meanL[row] = meanL;
       }
-      __syncwarp();
-      continue;
     }
-    int64_t act = bidx;
-    if ((uint64_t)a.u_explore[row] < a.thr) {
-      const int64_t nv = sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
-      const int64_t k = (int64_t)__umul64hi(a.u_action[row], (uint64_t)nv);
-      act = sp.seq ? seq_kth(sp, tb, sched, k) : pwarp_kth_valid(sp, tb, sched, k);
-    } else if (bidx == INT64_MAX) {
-      // a state always has a valid action, so no maximiser means non-finite Q values (NaN
-      // weights): flag it for hrp_sync and keep the environment consistent with the lowest
-      // valid action
-      if (lane == 0) atomicOr(a.err, 1u);
-      act = sp.seq ? seq_kth(sp, tb, sched, 0) : pwarp_kth_valid(sp, tb, sched, 0);
-    }
-    const uint8_t* wr = a.win + (size_t)row * W;
-    int64_t slot = 0;
-    int d = 0;
-    if (lane == 0) {
-      int g[4], sg[4], jobs[4];
-      const int l = decode_action(sp, act, g, sg);
-      const int C = tb.nsl[l];
-      int64_t solo;
-      const int64_t cr = corun_time(sp, pool, wr, l, g, sg, solo, jobs);
-      double r = ((double)solo / (double)cr - 1.0) * 100.0;
-      if (a.lam != 0.f) {
-        int64_t sc = 0, sm = 0, sT = 0;
-        for (int j = 0; j < W; ++j) { sc += pool.c[wr[j]]; sm += pool.m[wr[j]]; sT += pool.T[wr[j]]; }
-        const double cb = (double)sc / W, mb = (double)sm / W, Tb = (double)sT / W;
-        double ri = 0.0;
-        for (int k = 0; k < C; ++k) {
-          const uint32_t sl = sp.lay_slot[l * 4 + k];
-          const int p = jobs[k];
-          const double dr = (double)pool.T[p] / Tb;
-          ri += ((double)(sl & 0xffff) / 800.0 * ((double)pool.c[p] / cb) +
-                 (double)((sl >> 16) & 255) / 8.0 * ((double)pool.m[p] / mb)) * dr * dr;
-        }
-        r += (double)a.lam * ri;
-      }
-      const float meanLq = meanL;
-      int64_t q = fixed_point(z[0]) + fixed_point(z[1 + l] - meanLq);
-      uint64_t gm = 0;
-      const uint32_t ty = tb.stype[l];
-      for (int i = 0; i < C; ++i) {
-        if (!sp.seq) q += Fj(sp, z, w.meanJ, g[i], (ty >> (8 * sg[i])) & 255);
-        gm |= 1ull << g[i];
-      }
-      const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
-      const uint64_t s2 = sched | gm;
-      d = s2 == all;
-      slot = (a.t_step * (int64_t)a.M + row) % a.N_rep;
-      a.rep_sched[2 * slot] = sched;       // s
-      a.rep_sched[2 * slot + 1] = s2;      // s' (the action's jobs scheduled)
-      a.rep_act[slot] = act;
-      a.rep_r[slot] = (float)r;
-      a.rep_done[slot] = (uint8_t)d;
-      a.actions[row] = act;
-      a.rewards[row] = (float)r;
-      a.done[row] = (uint8_t)d;
-      if (a.corun) a.corun[row] = cr;
-      if (a.qsel) a.qsel[row] = (float)((double)q * (1.0 / 4294967296.0));
-      if (a.greedy) a.greedy[row] = bidx == INT64_MAX ? -1 : bidx;
-      a.sched[row] = d ? 0ull : s2;
-    }
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    d = __shfl_sync(0xffffffffu, d, 0);
-    uint8_t* wm = a.win + (size_t)row * W;
-    for (int j = lane; j < W; j += 32) a.rep_win[slot * W + j] = wm[j];
-    __syncwarp();
-    if (d)
-      for (int j = lane; j < W; j += 32) wm[j] = a.next_win[(size_t)row * W + j];
     __syncwarp();
   }
   if (a.n_evals) {
@@ -855,6 +980,18 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     // valid actions covered by the exact argmax (warp-uniform count), two counters on
     if (lane == 0 && ncovered) atomicAdd(a.n_evals + 2, (unsigned long long)ncovered);
   }
+}
+
+// a5-a7 after sel_kernel's greedy argmax (SEL_STEP): one warp per row, tables in global memory.
+__global__ void __launch_bounds__(256) sel_tail_kernel(DevSpace sp, DevPool pool, SelArgs a) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= a.M) return;
+  PTabs tg{};
+  tg.off = const_cast<int64_t*>(sp.off);
+  tg.stype = const_cast<uint32_t*>(sp.lay_stype);
+  tg.nsl = const_cast<uint8_t*>(sp.lay_n);
+  sel_tail(sp, pool, tg, a, row, a.z + (size_t)row * sp.H, a.g_meanL[row], a.sched[row],
+           a.g_best[row], a.g_bidx[row]);
 }
 
 // Action idx -> layout, members g_i and their slot types t_i (returns l; C = nsl[l]).
@@ -922,7 +1059,7 @@ __device__ inline float pwarp_qdesc(const int* __restrict__ d, const float* __re
 // (y = r when done), delta = Q(s, a) - y; dsq = delta^2, hdesc word 0 = delta / (B world).  The
 // last block to finish (ticket counter, reset by that block) reduces the loss = sum dsq / (2B)
 // exactly as loss_kernel does (256 threads, strided partial sums, block tree): same bits.
-__global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
+__global__ void __launch_bounds__(256) tdq_kernel(DevSpace sp, TdArgs a) {
   __shared__ float red[32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31;
@@ -930,6 +1067,18 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
   if (b < a.B) {
     const int* td = a.tdesc + (size_t)b * 8;
     int* hd = a.hdesc + (size_t)b * 8;
+    {   // action descriptors of a (hdesc, also read by the head backward) and a* (tdesc)
+      PTabs tg{};
+      tg.stype = const_cast<uint32_t*>(sp.lay_stype);
+      tg.nsl = const_cast<uint8_t*>(sp.lay_n);
+      write_desc(sp, tg, a.bact[b], hd);
+      if (a.bdone[b] != 0) {
+        if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
+      } else {
+        write_desc(sp, tg, a.astar[b], a.tdesc + (size_t)b * 8);
+      }
+      __syncwarp();
+    }
     float y = a.br[b];
     if (td[2] >= 0)   // -1: done (no bootstrap); 0 job rows in the flat head
       y += a.gamma * pwarp_qdesc(td, a.ht_hi + (size_t)b * a.w, a.ht_lo + (size_t)b * a.w, a.Wt,
@@ -966,7 +1115,7 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
 }
 
 template <int X>
-__global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 : 4)) td_kernel(DevSpace sp, TdArgs a) {
+__global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 : 4)) td_kernel(DevSpace sp, TdArgs a) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   PWarpSmem w;
   PTabs tb = pload_tabs<X>(sp, smem_raw, w);
@@ -980,7 +1129,9 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
     // action descriptors (tdesc: a*, hdesc: a)
     if (!done) {
       const float* zn = a.z_all + (size_t)(a.B + b) * sp.H;
-      const float meanL = pwarp_means(sp, zn, w.meanJ);
+      const float meanL = (X <= 0 && !sp.seq)
+                              ? pwarp_means_top<X == 0 ? 1 : 4>(sp, zn, a.bsched[a.B + b], w)
+                              : pwarp_means(sp, zn, w.meanJ);
       int64_t best;
       greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
       ncovered += sp.seq ? seq_n_valid(sp, tb, a.bsched[a.B + b]) : n_valid(sp, a.bsched[a.B + b]);
@@ -990,13 +1141,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X == 0 ? 1 : (X == 4 ? 3 :
                        : pwarp_kth_valid(sp, tb, a.bsched[a.B + b], 0);
       }
     }
-    if (lane == 0 && a.astar) a.astar[b] = astar;
-    write_desc(sp, tb, a.bact[b], a.hdesc + (size_t)b * 8);
-    if (done) {
-      if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
-    } else {
-      write_desc(sp, tb, astar, a.tdesc + (size_t)b * 8);
-    }
+    if (lane == 0) a.astar[b] = astar;   // -1 when done; descriptors: tdq_kernel
     __syncwarp();
   }
   if (a.n_evals) {

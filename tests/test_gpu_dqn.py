@@ -147,6 +147,50 @@ def test_config4_pruned_q_forward_sampled():
     close(hd.cpu().numpy().ravel(), z_o.ravel(), what="head")
 
 
+@pytest.mark.parametrize("period", [1, 3, 20])
+def test_pruned_top_lists_with_tied_job_rows(period):
+    # config 4 (W = 64): the head's job-advantage rows (and biases) of position j are copies of
+    # position j mod period's, so every slot type has exact ties across positions.  period 1:
+    # all U free positions tie (longer candidate lists than kPCap -> the full-scan fallback);
+    # 3 and 20: mixed lists.  Ties must go to the lowest position (R15), as in the oracle.
+    from paper_2405_08754_b200.session import Session
+    cfg = synth.config(4)
+    pool = synth.make_pool(cfg.pool)
+    sc = cfg.space
+    osp = SP.build_space(sc.window, sc.cmax, sc.shares, sc.mig)
+    dims = QN.net_dims(osp, cfg.net)
+    th = synth.init_weights(dims).copy()
+    fi, H = dims[-2], dims[-1]
+    o = sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 2))
+    Wh = th[o:o + fi * H].reshape(H, fi)
+    bh = th[o + fi * H:o + fi * H + H]
+    L, T, W = osp.L, osp.T, osp.W
+    for j in range(period, W):
+        src = 1 + L + (j % period) * T
+        dst = 1 + L + j * T
+        Wh[dst:dst + T] = Wh[src:src + T]
+        bh[dst:dst + T] = bh[src:src + T]
+    sess = Session(cfg, pool, n_envs=64, batch=64, init_weights=th, argmax_mode=2, replay=1024)
+    orc = EV.OracleDQN(osp, pool, cfg.net, th, 64, 64, 1024, gamma=cfg.gamma, lr=cfg.lr,
+                       argmax="pruned", workers=0)
+    wins, sched = _states(pool, 24, W, 11)
+    sched = sched.copy()
+    sched[:4] = 0                       # all 64 positions free
+    dw = torch.from_numpy(wins).to(sess.dev)
+    ds = torch.from_numpy(sched.view(np.int64)).to(sess.dev)
+    am, qm, hd = sess.q_forward(dw, ds, head=True)
+    torch.cuda.synchronize()
+    h = hd.cpu().numpy()
+    aj = h[:, 1 + L:].reshape(len(wins), W, T)
+    assert (aj[:, period:] == aj[:, [j % period for j in range(period, W)]]).all(), \
+        "tied rows must give bit-identical head outputs"
+    a_o, q_o, _ = orc.q_forward(wins, sched, gpu_argmax=am.cpu().numpy())
+    orc.close()
+    np.testing.assert_array_equal(am.cpu().numpy(), a_o)
+    close(qm.cpu().numpy(), q_o, what="qmax")
+    assert orc.near_ties == 0
+
+
 def test_double_dqn_hand_computed_through_libhrp():
     # the hand-computed double-DQN case of tests/test_oracle_dqn.py
     # through the C ABI: online and target heads differ, gamma = 0.9, s' not terminal
