@@ -221,11 +221,14 @@ __device__ __forceinline__ void ptop_type(const float* __restrict__ col, int T, 
     h = fmaxf(b2, v); v = fminf(b2, v); b2 = h;
     b3 = fmaxf(b3, v);
   }
-  const float thr = b3 == ninf ? ninf : f_as_float(b3 - mj);
+  // F(d) >= thrF needs d 2^32 >= thrF - 1/2 > thrF - 1 >= fl(thrF - 1) (for |thrF| >= 2^24 there
+  // is no float in (thrF - 1/2, thrF)), so d = fl(x - mean) >= fl(thrF - 1) 2^-32 keeps every
+  // position with F >= thrF (a superset: the insertion below uses the exact F)
+  const float thrd = b3 == ninf ? ninf : (f_as_float(b3 - mj) - 1.f) * 2.3283064365386963e-10f;
   uint64_t cm = 0;
 #pragma unroll
   for (int u = 0; u < NU; ++u)
-    if (f_as_float(x[u] - mj) >= thr) cm |= 1ull << u;
+    if (x[u] - mj >= thrd) cm |= 1ull << u;
   cm &= freem;
   if (!tv) return;
   w.meanJ[t] = mj;
@@ -665,48 +668,46 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   const int64_t Fv = fixed_point(z[0]);
   best = INT64_MIN;
   bidx = INT64_MAX;
-  // Seed: per layout the first leaf of its search (slot k takes its best Top-list job not
-  // already taken) -- a valid action, so (best, bidx) may start at the warp's best seed; the
-  // bound then prunes most layouts at the first level.
-  int64_t sv = INT64_MIN;
+  // Seed: the search's first-level bound UB(l) = base(l) + sum_k (best Top value of slot k's
+  // type) per layout; each lane takes its highest-UB layout (ties: lowest l) and builds that
+  // layout's greedy leaf (slot k takes its best Top-list job not already taken -- valid, since
+  // every list holds min(U, 4) >= C jobs), so (best, bidx) starts at a valid action close to the
+  // maximum and the bound prunes most layouts at the first level.
+  int64_t ubm = INT64_MIN;
   int sl = INT32_MAX;
-  int sjs[4] = {0, 0, 0, 0};
   for (int i = lane; i < sp.L; i += 32) {
     const int l = tb.lay_of_c[i];
     const int C = tb.nsl[l];
     const uint32_t ty = tb.stype[l];
-    int js[4] = {0, 0, 0, 0};
-    int64_t v = Fv + fixed_point(z[1 + l] - meanL);
-    bool ok = true;
+    if (w.top[(ty & 255) * 4 + C - 1] < 0) continue;   // U < C (every list has min(U, 4))
+    int64_t ub = Fv + fixed_point(z[1 + l] - meanL);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {          // constant indices: js stays in registers
-      if (k >= C || !ok) break;
-      const int t = (ty >> (8 * k)) & 255;
-      ok = false;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = w.top[t * 4 + q];
-        if (j < 0) break;
-        bool used = false;
-#pragma unroll
-        for (int k2 = 0; k2 < k; ++k2) used |= js[k2] == j;
-        if (!used) { js[k] = j; v += w.topv[t * 4 + q]; ok = true; break; }
-      }
-    }
-    // the lane's best seed by (value desc, layout asc) = (value desc, action index asc): only
-    // that one is ranked
-    if (!ok || v < sv || (v == sv && l > sl)) continue;
-    sv = v;
-    sl = l;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) sjs[k] = js[k];
+    for (int k = 0; k < 4; ++k)
+      if (k < C) ub += w.topv[((ty >> (8 * k)) & 255) * 4];
+    if (ub > ubm || (ub == ubm && l < sl)) { ubm = ub; sl = l; }
   }
   if (sl < sp.L) {
     const int C = tb.nsl[sl];
-    if (C == 1) pleaf<1>(tb, sl, W, sjs, sv, best, bidx);
-    else if (C == 2) pleaf<2>(tb, sl, W, sjs, sv, best, bidx);
-    else if (C == 3) pleaf<3>(tb, sl, W, sjs, sv, best, bidx);
-    else pleaf<4>(tb, sl, W, sjs, sv, best, bidx);
+    const uint32_t ty = tb.stype[sl];
+    int js[4] = {0, 0, 0, 0};
+    int64_t v = Fv + fixed_point(z[1 + sl] - meanL);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {          // constant indices: js stays in registers
+      if (k >= C) break;
+      const int t = (ty >> (8 * k)) & 255;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = w.top[t * 4 + q];
+        bool used = false;
+#pragma unroll
+        for (int k2 = 0; k2 < k; ++k2) used |= js[k2] == j;
+        if (!used) { js[k] = j; v += w.topv[t * 4 + q]; break; }
+      }
+    }
+    if (C == 1) pleaf<1>(tb, sl, W, js, v, best, bidx);
+    else if (C == 2) pleaf<2>(tb, sl, W, js, v, best, bidx);
+    else if (C == 3) pleaf<3>(tb, sl, W, js, v, best, bidx);
+    else pleaf<4>(tb, sl, W, js, v, best, bidx);
   }
   warp_best(best, bidx);
   // Exhaustive pruned search, lanes over layouts grouped by slot count (C-uniform rounds).
