@@ -120,17 +120,33 @@ __device__ __forceinline__ int64_t rank_comb(const int* g, int C, int W) {
   return r;
 }
 
+// Inverse of rank_comb.  Member i (k = C - 1 - i members after it) is the smallest v >= v0 whose
+// cumulative count sum_{u=v0..v} binom(W - 1 - u, k) = binom(W - v0, k + 1) - binom(W - 1 - v,
+// k + 1) (hockey stick) exceeds r: a binary search over v (binom(W - 1 - v, k + 1) decreases).
 __device__ __forceinline__ void unrank_comb(int64_t r, int W, int C, int* g) {
-  int v = 0;
+  int v0 = 0;
   for (int i = 0; i < C; ++i) {
-    while (true) {
-      int64_t c = c_binom[W - 1 - v][C - 1 - i];
-      if (r < c) break;
-      r -= c;
-      ++v;
+    const int k = C - 1 - i;
+    const int64_t tot = c_binom[W - v0][k + 1];
+    const int64_t R = tot - r;
+    int lo = v0, hi = W - 1 - k;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (c_binom[W - 1 - mid][k + 1] < R) hi = mid;
+      else lo = mid + 1;
     }
-    g[i] = v++;
+    g[i] = lo;
+    r -= tot - c_binom[W - lo][k + 1];
+    v0 = lo + 1;
   }
+}
+
+// Position of the n-th (0-based) set bit of m.
+__device__ __forceinline__ int nth_bit64(uint64_t m, int n) {
+  const uint32_t lo = (uint32_t)m;
+  const int pl = __popc(lo);
+  if (n < pl) return (int)__fns(lo, 0, n + 1);
+  return 32 + (int)__fns((uint32_t)(m >> 32), 0, n - pl + 1);
 }
 
 __device__ __forceinline__ int lehmer(const int* s, int C) {

@@ -190,19 +190,21 @@ __device__ __forceinline__ float f_as_float(float x) {
 // 64-bit candidate mask (no divergent work per position); the few candidates are then inserted
 // in ascending position order by (F desc, j asc) -- the Top-4 of the full scan, ties included
 // (with heavy ties the mask simply holds more positions).
-template <int NJ>
-__device__ __forceinline__ void ptop_type(const float* __restrict__ col, int T, int W,
+// FULL: W == 16 NJ (compile-time trip counts; col points at a valid column in every lane).
+template <int NJ, bool FULL>
+__device__ __forceinline__ void ptop_type(const float* __restrict__ col, int T, int Wr,
                                           uint64_t freem, int t, bool tv, PWarpSmem& w) {
   constexpr int NU = 16 * NJ;
+  const int W = FULL ? NU : Wr;
   const float ninf = -INFINITY;
   const int w4 = (W >> 2) << 2;
   float x[NU];
 #pragma unroll
-  for (int u = 0; u < NU; ++u) x[u] = (tv && u < W) ? col[u * T] : 0.f;
+  for (int u = 0; u < NU; ++u) x[u] = (FULL || u < W) ? col[u * T] : 0.f;
   float s[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int u = 0; u < NU; ++u) {   // chunks of 4 into s0..s3, the W % 4 tail into s0 (ascending)
-    if (u < w4) s[u & 3] += x[u];
+    if (FULL || u < w4) s[u & 3] += x[u];
     else if (u < W) s[0] += x[u];
   }
   const float mj = ((s[0] + s[1]) + (s[2] + s[3])) / (float)W;
@@ -270,7 +272,8 @@ __device__ inline float pwarp_means_top(const DevSpace& sp, const float* __restr
     const int t = t0 + lane;
     const bool tv = t < T;
     const float* col = aJ + (tv ? t : 0);
-    ptop_type<NJ>(col, T, W, freem, t, tv, w);
+    if (W == 16 * NJ) ptop_type<NJ, true>(col, T, W, freem, t, tv, w);
+    else ptop_type<NJ, false>(col, T, W, freem, t, tv, w);
   }
   __syncwarp();
   return meanL;
@@ -802,14 +805,16 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
   const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
   const uint64_t freem = all & ~sched;
   const int U = __popcll(freem);
+  // valid actions of a C-slot layout: U (U - 1) .. (U - C + 1) ordered member choices
+  const int64_t p1 = U, p2 = p1 * (U - 1), p3 = U >= 2 ? p2 * (U - 2) : 0,
+                p4 = U >= 3 ? p3 * (U - 3) : 0;
   for (int l0 = 0; l0 < sp.L; l0 += 32) {
     const int l = l0 + lane;
     int64_t cnt = 0;
     int C = 0;
     if (l < sp.L) {
       C = tb.nsl[l];
-      cnt = 1;
-      for (int i = 0; i < C; ++i) cnt *= (U - i);
+      cnt = C == 1 ? p1 : C == 2 ? p2 : C == 3 ? p3 : p4;
       if (U < C) cnt = 0;
     }
     int64_t incl = cnt;  // inclusive scan
@@ -829,11 +834,7 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
         const int64_t rg = kk / f, rs = kk - rg * f;
         int gp[4], g[4];
         unrank_comb(rg, U, C, gp);
-        for (int i = 0; i < C; ++i) {
-          uint64_t m = freem;
-          for (int x = 0; x < gp[i]; ++x) m &= m - 1;
-          g[i] = __ffsll((long long)m) - 1;
-        }
+        for (int i = 0; i < C; ++i) g[i] = nth_bit64(freem, gp[i]);
         res = tb.off[l] + rank_comb(g, C, W) * f + rs;
       }
       return __shfl_sync(0xffffffffu, res, src);
