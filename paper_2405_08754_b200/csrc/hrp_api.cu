@@ -285,6 +285,7 @@ struct hrp_ctx {
   int64_t* bastar = nullptr;          // [B] a* when the caller passes none
   int64_t *g_best = nullptr, *g_bidx = nullptr;   // [rows_max] sel_kernel -> sel_tail_kernel
   float* g_meanL = nullptr;
+  float* g_meanJ = nullptr;           // [rows_max][T]
   double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
   float *hc0 = nullptr, *hmT = nullptr;      // online head duelling-mean rows [w + 1], [T][w + 1]
   float *hc0t = nullptr, *hmTt = nullptr;    // target head
@@ -604,6 +605,7 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.g_best = c->g_best;
   a.g_bidx = c->g_bidx;
   a.g_meanL = c->g_meanL;
+  a.g_meanJ = c->g_meanJ;
 #define HRP_SEL(X) sel_kernel<X><<<grid, pwarps(X > 0) * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
   HRP_VARIANT(c->sel_variant, HRP_SEL);
 #undef HRP_SEL
@@ -853,6 +855,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     CK(ar.alloc((void**)&c->g_best, sizeof(int64_t) * (size_t)c->rows_max));
     CK(ar.alloc((void**)&c->g_bidx, sizeof(int64_t) * (size_t)c->rows_max));
     CK(ar.alloc((void**)&c->g_meanL, sizeof(float) * (size_t)c->rows_max));
+    CK(ar.alloc((void**)&c->g_meanJ, sizeof(float) * (size_t)c->rows_max * std::max(1, T)));
     CK(ar.alloc((void**)&c->hacc, sizeof(double) * (size_t)H * (wd + 1)));
     CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)(T + 1) * (wd + 1)));
     CK(ar.alloc((void**)&c->hc0, sizeof(float) * (wd + 1)));

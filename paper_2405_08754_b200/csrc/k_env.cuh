@@ -218,6 +218,7 @@ struct SelArgs {
   int64_t* g_best;              // [M] SEL_STEP: the greedy argmax per row (sel_kernel ->
   int64_t* g_bidx;              //     sel_tail_kernel)
   float* g_meanL;
+  float* g_meanJ;               // [M][T] slot-type means
 };
 
 // ---------------------------------------------------------------------------------------

@@ -871,26 +871,11 @@ __device__ inline void sel_tail(const DevSpace& sp, const DevPool& pool, const P
   const int l = decode_action(sp, act, g, sg);   // every lane (same result)
   const int C = tb.nsl[l];
   const uint32_t ty = tb.stype[l];
-  // slot-type means of the action's members, summed from the head row in pwarp_means' order
-  // (same bits): lane 4i + q sums s_q of member i's type
+  // slot-type means of the action's members (sel_kernel's, written per row), for Q of an
+  // exploratory action (a greedy action's Q is the argmax's exact score)
   float mjv[4] = {0.f, 0.f, 0.f, 0.f};
-  if (!sp.seq) {
-    const int i = lane >> 2, q = lane & 3;
-    const int T = sp.T, w4 = (W >> 2) << 2;
-    float sq = 0.f;
-    if (i < C) {
-      const float* aJ = z + 1 + sp.L + ((ty >> (8 * sg[i])) & 255);
-      for (int j = q; j < w4; j += 4) sq += aJ[j * T];
-      if (q == 0)
-        for (int j = w4; j < W; ++j) sq += aJ[j * T];
-    }
-    const float s1 = __shfl_down_sync(0xffffffffu, sq, 1);
-    const float s2 = __shfl_down_sync(0xffffffffu, sq, 2);
-    const float s3 = __shfl_down_sync(0xffffffffu, sq, 3);
-    const float mj = ((sq + s1) + (s2 + s3)) / (float)W;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) mjv[k] = __shfl_sync(0xffffffffu, mj, 4 * k);
-  }
+  if (!sp.seq && act != bidx)
+    for (int i = 0; i < C; ++i) mjv[i] = a.g_meanJ[(size_t)row * sp.T + ((ty >> (8 * sg[i])) & 255)];
   if (lane == 0) {
     int jobs[4];
     int64_t solo;
@@ -910,13 +895,15 @@ __device__ inline void sel_tail(const DevSpace& sp, const DevPool& pool, const P
       }
       r += (double)a.lam * ri;
     }
-    int64_t q = fixed_point(z[0]) + fixed_point(z[1 + l] - meanL);
-    uint64_t gm = 0;
-    for (int i = 0; i < C; ++i) {
-      if (!sp.seq)
-        q += fixed_point(z[1 + sp.L + g[i] * sp.T + ((ty >> (8 * sg[i])) & 255)] - mjv[i]);
-      gm |= 1ull << g[i];
+    int64_t q = best;
+    if (act != bidx) {
+      q = fixed_point(z[0]) + fixed_point(z[1 + l] - meanL);
+      for (int i = 0; i < C; ++i)
+        if (!sp.seq)
+          q += fixed_point(z[1 + sp.L + g[i] * sp.T + ((ty >> (8 * sg[i])) & 255)] - mjv[i]);
     }
+    uint64_t gm = 0;
+    for (int i = 0; i < C; ++i) gm |= 1ull << g[i];
     const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
     const uint64_t s2 = sched | gm;
     d = s2 == all;
@@ -959,6 +946,10 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
     const uint64_t sched = a.sched[row];
     const float meanL = (X <= 0 && !sp.seq) ? pwarp_means_top<X == 0 ? 1 : 4>(sp, z, sched, w)
                                             : pwarp_means(sp, z, w.meanJ);
+    if (a.mode == SEL_STEP && !sp.seq) {   // for sel_tail_kernel (Q of exploratory actions)
+      __syncwarp();
+      for (int t = lane; t < sp.T; t += 32) a.g_meanJ[(size_t)row * sp.T + t] = w.meanJ[t];
+    }
     int64_t best, bidx;
     greedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
     ncovered += sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
