@@ -18,7 +18,8 @@ def klass(name):
     m = re.search(r"tc_gemm_kernel<\s*(\d+),\s*(\d+),\s*(\d+)", name)
     if m:
         return "gemm_fwd" if int(m.group(3)) in (0, 1) else "gemm_bwd"
-    for key, cls in (("encode_kernel", "encode"), ("sel_kernel", "select"), ("td_kernel", "td"),
+    for key, cls in (("encode_kernel", "encode"), ("sel_kernel", "select"),
+                     ("sel_tail_kernel", "select"), ("td_kernel", "td"), ("tdq_kernel", "td"),
                      ("sample_kernel", "sample"), ("sgd", "sgd"), ("split_kernel", "sgd"),
                      ("split_t_kernel", "sgd"), ("reduce_splits", "gemm_bwd"),
                      ("rowsum", "gemm_bwd"), ("transpose_kernel", "gemm_bwd"),
