@@ -353,14 +353,28 @@ def run_gpu(args, cfg):
         # per-kernel breakdown: a separate pass over the same step inputs with per-launch CUDA
         # events on the context's stream (kept out of the timed region above: the extra
         # event records perturb a ~1 ms step)
+        # (with --graph the profiled steps are captured too, event records included, so the
+        # per-launch intervals hold GPU time only, not host launch gaps of eager submission)
         hrp.hrp_profile(sess.ctx, True)
+        pgraphs = []
+        if args.graph:
+            for k in range(args.steps):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    one_step(args.warmup + k, streams_d[args.warmup + k])
+                pgraphs.append(g)
+            stream.synchronize()
         for k in range(args.steps):
             t = args.warmup + k
             flush.zero_()
-            one_step(t, streams_d[t])
+            if args.graph:
+                pgraphs[k].replay()
+            else:
+                one_step(t, streams_d[t])
         stream.synchronize()
         prof = hrp.hrp_profile_read(sess.ctx)
         hrp.hrp_profile(sess.ctx, False)
+        del pgraphs
     # max over ranks
     ms = parallel.max_over_ranks(ms, dev)
     value = world * E * args.steps / (ms / 1e3)     # all ranks' env-steps / slowest rank's time

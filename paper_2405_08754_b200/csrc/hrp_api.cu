@@ -361,7 +361,9 @@ void prof_begin(hrp_ctx* c) {
   c->ev_begin = nullptr;
   if (!c->prof) return;
   c->ev_begin = prof_event(c);
-  if (c->ev_begin) cudaEventRecord(c->ev_begin, c->stream);
+  // external record: inside a stream capture this becomes an event-record node of the graph,
+  // so the profiled launches can be replayed from a graph and still timed
+  if (c->ev_begin) cudaEventRecordWithFlags(c->ev_begin, c->stream, cudaEventRecordExternal);
 }
 
 hrp_status launch_check(hrp_ctx* c, int cls) {
@@ -371,7 +373,7 @@ hrp_status launch_check(hrp_ctx* c, int cls) {
   if (c->prof && c->ev_begin) {
     cudaEvent_t end = prof_event(c);
     if (end) {
-      cudaEventRecord(end, c->stream);
+      cudaEventRecordWithFlags(end, c->stream, cudaEventRecordExternal);
       c->prof_rec.push_back({cls, {c->ev_begin, end}});
     }
     c->ev_begin = nullptr;
