@@ -77,15 +77,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// K-major operand tile of `rows` x 128 B in SWIZZLE_128B layout (8-row atoms of 1024 B).
+// K-major operand tile of `rows` x (4 BKT) B: BKT = 32 fp32 per row in SWIZZLE_128B layout
+// (8-row atoms of 1024 B), BKT = 16 in SWIZZLE_64B (8-row atoms of 512 B).
+template <int BKT>
 __device__ __forceinline__ uint64_t smem_desc(const void* p) {
   const uint64_t addr = smem_u32(p);
   uint64_t d = 0;
   d |= (addr >> 4) & 0x3FFF;          // start address
-  // LBO = 0: unused for swizzled K-major with one 128-B atom along K
-  d |= (uint64_t)(1024 >> 4) << 32;   // SBO: 8 rows x 128 B
+  // LBO = 0: unused for swizzled K-major with one atom along K
+  d |= (uint64_t)((8 * 4 * BKT) >> 4) << 32;    // SBO: 8 rows
   d |= (uint64_t)1 << 46;             // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
+  d |= (uint64_t)(BKT == 32 ? 2 : 4) << 61;     // SWIZZLE_128B / SWIZZLE_64B
   return d;
 }
 
@@ -130,10 +132,10 @@ __device__ __forceinline__ float tf32_rna(float x) {
         "=r"(v[31])                                                                           \
       : "r"(taddr))
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int BKT = BK>
 struct TcSmem {
-  static constexpr int A_BYTES = BM * BK * 4;   // 16 KB
-  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int A_BYTES = BM * BKT * 4;   // 16 KB at BKT = 32
+  static constexpr int B_BYTES = BN * BKT * 4;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A hi, A lo, B hi, B lo
   static constexpr int TOTAL = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align*/;
 };
@@ -183,13 +185,15 @@ __device__ __forceinline__ void store_split(float* p, float* plo, float v) {
   }
 }
 
-// mapA0/mapA1: A hi/lo planes; mapB0/mapB1: B hi/lo planes.
-template <int BN, int STAGES, int EPI>
+// mapA0/mapA1: A hi/lo planes; mapB0/mapB1: B hi/lo planes.  BKT: fp32 per K block (32:
+// 128-B rows, SWIZZLE_128B; 16: 64-B rows, SWIZZLE_64B -- twice the stages in the same shared
+// memory, for the 256-wide tiles).
+template <int BN, int STAGES, int EPI, int BKT = BK>
 __global__ void __launch_bounds__(kThreadsTc, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
                const TcArgs a) {
-  using S = TcSmem<BN, STAGES>;
+  using S = TcSmem<BN, STAGES, BKT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto a_hi = [&](int s) { return smem + s * S::STAGE_BYTES; };
@@ -206,7 +210,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int kbeg = blockIdx.z * a.kc;
   const int kend = min(a.K, kbeg + a.kc);
-  const int nk = (kend - kbeg + BK - 1) / BK;
+  const int nk = (kend - kbeg + BKT - 1) / BKT;
   if (threadIdx.x == 0) TRACE(0);
 
   if (warp == 0 && lane == 0) {
@@ -239,12 +243,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)((a.fast ? 1 : 2) * (a.boxA + a.boxB)) * BK * 4;
+      const uint32_t bytes = (uint32_t)((a.fast ? 1 : 2) * (a.boxA + a.boxB)) * BKT * 4;
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty_bar[s], ((kb / STAGES) - 1) & 1);
         mbar_expect_tx(&full_bar[s], bytes);
-        const int kk = kbeg + kb * BK;
+        const int kk = kbeg + kb * BKT;
         tma_load_2d(a_hi(s), &mapA0, &full_bar[s], kk, m0);
         tma_load_2d(b_hi(s), &mapB0, &full_bar[s], kk, n0);
         if (!a.fast) {
@@ -265,13 +269,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
         const int s = kb % STAGES;
         mbar_wait(&full_bar[s], (kb / STAGES) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint64_t dah = smem_desc(a_hi(s)), dal = smem_desc(a_lo(s));
-        const uint64_t dbh = smem_desc(b_hi(s)), dbl = smem_desc(b_lo(s));
+        const uint64_t dah = smem_desc<BKT>(a_hi(s)), dal = smem_desc<BKT>(a_lo(s));
+        const uint64_t dbh = smem_desc<BKT>(b_hi(s)), dbl = smem_desc<BKT>(b_lo(s));
         const int mi = kb % a.nmain;
         const uint32_t t_main = tmem + (uint32_t)(mi * BN);
         const uint32_t t_c = a.ncorr ? t_corr : t_main;
 #pragma unroll
-        for (int k = 0; k < BK / 8; ++k) {
+        for (int k = 0; k < BKT / 8; ++k) {
           const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // 32 B per K=8 step
           const uint32_t accm = (kb >= a.nmain || k > 0) ? 1u : 0u;
           const uint32_t accc = a.ncorr ? ((kb > 0 || k > 0) ? 1u : 0u) : 1u;
@@ -524,14 +528,17 @@ bool get_encode() {
 }
 
 // 2D fp32 row-major [rows][cols] map (row stride ld elements, ld % 4 == 0) with a
-// 32 x box_rows box, SWIZZLE_128B; columns beyond cols read as zero.
-bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int ld, int box_rows) {
+// bk x box_rows box, SWIZZLE_128B (bk = 32) or SWIZZLE_64B (bk = 16); columns beyond cols read
+// as zero.
+bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int ld, int box_rows,
+              int bk = BK) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") rows " +
@@ -544,7 +551,7 @@ bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int ld, int bo
 
 int g_acc_mode = 2;   // 0: one accumulator; 1: main + correction; 2: up to 3 mains + correction
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int STAGES, int EPI, int BKT = BK>
 hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   CUtensorMap ma0, ma1, mb0, mb1;
   a.ncorr = (g_acc_mode >= 1 && !a.fast) ? 1 : 0;
@@ -558,18 +565,18 @@ hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   // boxes never exceed the tensor; rows of a tile beyond the box only feed masked outputs
   a.boxA = std::min(BM, a.M);
   a.boxB = std::min(BN, a.N);
-  if (!make_map(&ma0, A.hi, a.M, a.K, a.lda, a.boxA) ||
-      !make_map(&ma1, A.lo, a.M, a.K, a.lda, a.boxA) ||
-      !make_map(&mb0, B.hi, a.N, a.K, a.ldb, a.boxB) ||
-      !make_map(&mb1, B.lo, a.N, a.K, a.ldb, a.boxB))
+  if (!make_map(&ma0, A.hi, a.M, a.K, a.lda, a.boxA, BKT) ||
+      !make_map(&ma1, A.lo, a.M, a.K, a.lda, a.boxA, BKT) ||
+      !make_map(&mb0, B.hi, a.N, a.K, a.ldb, a.boxB, BKT) ||
+      !make_map(&mb1, B.lo, a.N, a.K, a.ldb, a.boxB, BKT))
     return HRP_ECUDA;
-  constexpr int smem = TcSmem<BN, STAGES>::TOTAL;
+  constexpr int smem = TcSmem<BN, STAGES, BKT>::TOTAL;
   // the attribute belongs to the device context: track it per device
   static bool attr[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI>,
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES, EPI, BKT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
     attr[dev & 63] = true;
@@ -585,7 +592,7 @@ hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES, EPI>, ma0, ma1, mb0, mb1, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES, EPI, BKT>, ma0, ma1, mb0, mb1, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
@@ -609,6 +616,9 @@ void tc_gemm_destroy(TcGemm* g) { delete g; }
 bool tc_gemm_supported(int M, int N, int K) { return M >= 1 && N >= 1 && K >= 1; }
 
 int g_force_bn = 0;  // diagnostics: force the tile width (64 / 128 / 256), 0 = heuristic
+// 256-wide tiles: 4 stages of 16-fp32 K blocks (SWIZZLE_64B) instead of 2 of 32 (HRP_BK32=1 for
+// the 2-stage variant, a diagnostic A/B switch)
+static const bool g_bk16 = !std::getenv("HRP_BK32");
 
 static int pick_bn(int M, int N, int K, int nsm) {
   if (g_force_bn == 64 || g_force_bn == 128 || g_force_bn == 256) return g_force_bn;
@@ -629,7 +639,8 @@ static int pick_bn(int M, int N, int K, int nsm) {
 
 template <int EPI>
 static hrp_status run_bn(int bn, cudaStream_t st, Planes A, Planes B, const TcArgs& a) {
-  if (bn == 256) return launch<256, 2, EPI>(st, A, B, a, 1);
+  if (bn == 256) return g_bk16 ? launch<256, 4, EPI, 16>(st, A, B, a, 1)
+                                : launch<256, 2, EPI>(st, A, B, a, 1);
   if (bn == 128) return launch<128, 3, EPI>(st, A, B, a, 1);
   return launch<64, 4, EPI>(st, A, B, a, 1);
 }
