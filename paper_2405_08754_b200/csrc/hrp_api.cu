@@ -264,6 +264,7 @@ struct hrp_ctx {
   uint8_t* rep_win = nullptr;
   uint64_t* rep_sched = nullptr;
   int64_t* rep_act = nullptr;
+  int* rep_desc = nullptr;            // [N][8] action descriptors of the stored transitions
   float* rep_r = nullptr;
   uint8_t* rep_done = nullptr;
   int64_t t = 0, inserted = 0;
@@ -282,10 +283,10 @@ struct hrp_ctx {
   // dz, the head's two backward GEMMs become gathers / scatters
   int* hdesc = nullptr;               // [B][8]
   int* tdesc = nullptr;               // [B][8] (a* on s')
-  int64_t* bastar = nullptr;          // [B] a* when the caller passes none
   int64_t *g_best = nullptr, *g_bidx = nullptr;   // [rows_max] sel_kernel -> sel_tail_kernel
   float* g_meanL = nullptr;
   float* g_meanJ = nullptr;           // [rows_max][T]
+  int64_t* g_pk = nullptr;            // [rows_max]
   double *hacc = nullptr, *haccU = nullptr;  // [H][w + 1], [T][w + 1]
   float *hc0 = nullptr, *hmT = nullptr;      // online head duelling-mean rows [w + 1], [T][w + 1]
   float *hc0t = nullptr, *hmTt = nullptr;    // target head
@@ -608,6 +609,8 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.g_bidx = c->g_bidx;
   a.g_meanL = c->g_meanL;
   a.g_meanJ = c->g_meanJ;
+  a.g_pk = c->g_pk;
+  a.rep_desc = c->rep_desc;
 #define HRP_SEL(X) sel_kernel<X><<<grid, pwarps(X > 0) * 32, c->p_smem, c->stream>>>(c->dt.sp, c->dt.pool, a)
   HRP_VARIANT(c->sel_variant, HRP_SEL);
 #undef HRP_SEL
@@ -809,6 +812,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(ar.alloc((void**)&c->rep_win, N * W));
   CK(ar.alloc((void**)&c->rep_sched, N * 16));  // [N][2]: s and s' scheduled masks
   CK(ar.alloc((void**)&c->rep_act, N * 8));
+  CK(ar.alloc((void**)&c->rep_desc, N * 32));
   CK(ar.alloc((void**)&c->rep_r, N * 4));
   CK(ar.alloc((void**)&c->rep_done, N));
   c->Bp = r4(B);
@@ -853,10 +857,10 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     const int T = hs.T;
     CK(ar.alloc((void**)&c->hdesc, sizeof(int) * 8 * (size_t)B));
     CK(ar.alloc((void**)&c->tdesc, sizeof(int) * 8 * (size_t)B));
-    CK(ar.alloc((void**)&c->bastar, sizeof(int64_t) * (size_t)B));
     CK(ar.alloc((void**)&c->g_best, sizeof(int64_t) * (size_t)c->rows_max));
     CK(ar.alloc((void**)&c->g_bidx, sizeof(int64_t) * (size_t)c->rows_max));
     CK(ar.alloc((void**)&c->g_meanL, sizeof(float) * (size_t)c->rows_max));
+    CK(ar.alloc((void**)&c->g_pk, sizeof(int64_t) * (size_t)c->rows_max));
     CK(ar.alloc((void**)&c->g_meanJ, sizeof(float) * (size_t)c->rows_max * std::max(1, T)));
     CK(ar.alloc((void**)&c->hacc, sizeof(double) * (size_t)H * (wd + 1)));
     CK(ar.alloc((void**)&c->haccU, sizeof(double) * (size_t)(T + 1) * (wd + 1)));
@@ -1041,7 +1045,8 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   // decode is latency-bound: 8 samples per 256-thread CTA spreads it over the SMs)
   sample_encode_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(
       c->dt.sp, c->dt.pool, B, d_u_replay, nf, c->rep_win, c->rep_sched, c->rep_act, c->rep_r,
-      c->rep_done, c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx, c->X.hi, c->X.lo,
+      c->rep_done, c->bwin, c->bsched, c->bact, c->br, c->bdone, d_sample_idx, c->rep_desc,
+      c->hdesc, c->X.hi, c->X.lo,
       c->ldX, c->XT.hi, c->XT.lo, c->Bp);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
   // online net on [s; s'] (activations of the s rows kept for backward) on the main stream,
@@ -1103,7 +1108,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
     t.w = hw;
   }
   t.dsq = c->dsq;
-  t.astar = d_astar ? d_astar : c->bastar;
+  t.astar = d_astar;
   t.n_evals = c->n_evals + 1;
   t.ctr = c->sched_ctr + 1;
   t.err = c->dev_err;
@@ -1119,7 +1124,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   t.loss = d_loss;
   t.done_ctr = c->sched_ctr + 2;
   prof_begin(c);
-  tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(c->dt.sp, t);
+  tdq_kernel<<<(B + 7) / 8, 256, 0, c->stream>>>(t);
   if ((s = launch_check(c, HRP_K_TD))) return s;
   return mlp_backward(c, B);
 }

@@ -219,6 +219,8 @@ struct SelArgs {
   int64_t* g_bidx;              //     sel_tail_kernel)
   float* g_meanL;
   float* g_meanJ;               // [M][T] slot-type means
+  int64_t* g_pk;                // [M] the maximiser's packed leaf (pack_leaf) or -1
+  int* rep_desc;                // [N_rep][8] the transition's action descriptor (words 1..7)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -237,6 +239,7 @@ sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restric
                      uint8_t* __restrict__ bwin, uint64_t* __restrict__ bsched,
                      int64_t* __restrict__ bact, float* __restrict__ br,
                      uint8_t* __restrict__ bdone, int64_t* __restrict__ out_idx,
+                     const int* __restrict__ rep_desc, int* __restrict__ hdesc,
                      float* __restrict__ X, float* __restrict__ Xlo, int ldx,
                      float* __restrict__ XT, float* __restrict__ XTlo, int ldt) {
   __shared__ __align__(16) float rows[8][kEncMaxIn];
@@ -248,6 +251,8 @@ sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restric
     const int64_t idx = (int64_t)(((uint64_t)u[b] * (uint64_t)n_filled) >> 32);
     const uint8_t* w = rep_win + idx * W;
     const uint64_t s = rep_sched[2 * idx], s2 = rep_sched[2 * idx + 1];
+    if (lane >= 1 && lane < 8)   // a's action descriptor (word 0: tdq_kernel's scale)
+      hdesc[(size_t)b * 8 + lane] = rep_desc[idx * 8 + lane];
     if (lane == 0) {
       bsched[b] = s;
       bsched[B + b] = s2;
@@ -297,7 +302,7 @@ struct TdArgs {
   int* hdesc;           // structured head gradient: [B][8] per sample
                         //   {sc bits, 1 + l, C, rows 1 + L + g_i T + t_i (i < C; -1 pad) x 4,
                         //    t_0 | t_1 << 8 | t_2 << 16 | t_3 << 24}, sc = delta / (B world)
-  int64_t* astar;       // [B] a* (-1 when done): td_kernel -> tdq_kernel
+  int64_t* astar;       // [B] optional: a* (-1 when done)
   // sparse Q: Q(s, a) and Q_target(s', a*) from the last hidden activations and the
   // head rows they need, Q = h . (c0 + W[1 + l] + sum_i (W[r_i] - mT[t_i])) + (same on biases),
   // instead of full online-head rows for s and target-head rows for s'

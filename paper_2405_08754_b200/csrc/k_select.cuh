@@ -568,9 +568,56 @@ __device__ inline void xgreedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w
 // Exact top-C pruned search (X = false)
 
 // Leaf of the assignment search: jobs j[k] on slots k of layout l with score v.
+// Packed leaf (layout l, job js[k] on slot k): l | js[0] << 16 | .. | js[3] << 40 (W <= 64).
+__device__ __forceinline__ int64_t pack_leaf(int l, const int (&js)[4]) {
+  return (int64_t)l | ((int64_t)js[0] << 16) | ((int64_t)js[1] << 24) | ((int64_t)js[2] << 32) |
+         ((int64_t)js[3] << 40);
+}
+
+// Members of a packed leaf in ascending job order (the action index's order): g_i, the slot
+// sg_i it takes and that slot's type t_i.  Returns l (C = nsl[l]).
+__device__ __forceinline__ int leaf_members(const PTabs& tb, int64_t pk, int* g, int* sg,
+                                            int* t) {
+  const int l = (int)(pk & 0xffff);
+  const int C = tb.nsl[l];
+  const uint32_t ty = tb.stype[l];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    g[k] = (int)((pk >> (16 + 8 * k)) & 255);
+    sg[k] = k;
+  }
+#pragma unroll
+  for (int i = 1; i < 4; ++i)          // insertion sort of (job, slot) by job, C <= 4
+#pragma unroll
+    for (int j = i; j > 0; --j)
+      if (j < C && g[j] < g[j - 1]) {
+        int u = g[j]; g[j] = g[j - 1]; g[j - 1] = u;
+        u = sg[j]; sg[j] = sg[j - 1]; sg[j - 1] = u;
+      }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t[i] = (ty >> (8 * sg[i])) & 255;
+  return l;
+}
+
+// Action descriptor words 1..7 (lanes 1..7) from an action's layout and ordered members (the
+// format of write_desc).
+__device__ __forceinline__ void desc_from_members(const DevSpace& sp, int l, int C, const int* g,
+                                                  const int* t, int* d) {
+  const int lane = threadIdx.x & 31;
+  if (lane >= 1 && lane < 8) {
+    int v;
+    if (lane == 1) v = 1 + l;
+    else if (lane == 2) v = sp.seq ? 0 : C;     // job-advantage rows (none in the flat head)
+    else if (lane < 7) v = lane - 3 < C ? 1 + sp.L + g[lane - 3] * sp.T + t[lane - 3] : -1;
+    else v = (t[0] & 255) | (C > 1 ? (t[1] & 255) << 8 : 0) | (C > 2 ? (t[2] & 255) << 16 : 0) |
+             (C > 3 ? (t[3] & 255) << 24 : 0);
+    d[lane] = v;
+  }
+}
+
 template <int C>
 __device__ __forceinline__ void pleaf(const PTabs& tb, int l, int W, const int (&js)[4], int64_t v,
-                                      int64_t& best, int64_t& bidx) {
+                                      int64_t& best, int64_t& bidx, int64_t& bpk) {
   // group g = sorted jobs; sigma(i) = slot of member g_i; index = off + rank(g) C! + lehmer
   int g[4], sg[4], rk_[4];
 #pragma unroll
@@ -605,7 +652,7 @@ __device__ __forceinline__ void pleaf(const PTabs& tb, int l, int W, const int (
   }
   constexpr int64_t fC = C == 1 ? 1 : C == 2 ? 2 : C == 3 ? 6 : 24;
   const int64_t idx = tb.off[l] + rk * fC + lc;
-  if (v > best || idx < bidx) { best = v; bidx = idx; }
+  if (v > best || idx < bidx) { best = v; bidx = idx; bpk = pack_leaf(l, js); }
 }
 
 // Depth-first search over the C^C Top-list assignments of one layout, values descending per
@@ -613,7 +660,7 @@ __device__ __forceinline__ void pleaf(const PTabs& tb, int l, int W, const int (
 template <int C>
 __device__ __forceinline__ void psearch(const PTabs& tb, const PWarpSmem& w, int l, int W,
                                         uint32_t ty, int64_t base, int64_t& best, int64_t& bidx,
-                                        int64_t& nevals) {
+                                        int64_t& bpk, int64_t& nevals) {
   int tk[4];
 #pragma unroll
   for (int k = 0; k < C; ++k) tk[k] = (ty >> (8 * k)) & 255;
@@ -630,21 +677,21 @@ __device__ __forceinline__ void psearch(const PTabs& tb, const PWarpSmem& w, int
     js[0] = w.top[tk[0] * 4 + q0];
     const int64_t v0 = base + w.topv[tk[0] * 4 + q0];
     if (v0 + ub[1] < best) break;
-    if (C == 1) { ++nevals; if (v0 >= best) pleaf<C>(tb, l, W, js, v0, best, bidx); continue; }
+    if (C == 1) { ++nevals; if (v0 >= best) pleaf<C>(tb, l, W, js, v0, best, bidx, bpk); continue; }
 #pragma unroll 1
     for (int q1 = 0; q1 < (C > 1 ? C : 1); ++q1) {
       js[1] = w.top[tk[1] * 4 + q1];
       const int64_t v1 = v0 + w.topv[tk[1] * 4 + q1];
       if (v1 + ub[2] < best) break;
       if (js[1] == js[0]) continue;
-      if (C == 2) { ++nevals; if (v1 >= best) pleaf<C>(tb, l, W, js, v1, best, bidx); continue; }
+      if (C == 2) { ++nevals; if (v1 >= best) pleaf<C>(tb, l, W, js, v1, best, bidx, bpk); continue; }
 #pragma unroll 1
       for (int q2 = 0; q2 < (C > 2 ? C : 1); ++q2) {
         js[2] = w.top[tk[2] * 4 + q2];
         const int64_t v2 = v1 + w.topv[tk[2] * 4 + q2];
         if (v2 + ub[3] < best) break;
         if (js[2] == js[0] || js[2] == js[1]) continue;
-        if (C == 3) { ++nevals; if (v2 >= best) pleaf<C>(tb, l, W, js, v2, best, bidx); continue; }
+        if (C == 3) { ++nevals; if (v2 >= best) pleaf<C>(tb, l, W, js, v2, best, bidx, bpk); continue; }
 #pragma unroll
         for (int q3 = 0; q3 < (C > 3 ? C : 1); ++q3) {
           js[3] = w.top[tk[3] * 4 + q3];
@@ -652,18 +699,30 @@ __device__ __forceinline__ void psearch(const PTabs& tb, const PWarpSmem& w, int
           if (v3 + ub[4] < best) break;
           if (js[3] == js[0] || js[3] == js[1] || js[3] == js[2]) continue;
           ++nevals;
-          if (v3 >= best) pleaf<C>(tb, l, W, js, v3, best, bidx);
+          if (v3 >= best) pleaf<C>(tb, l, W, js, v3, best, bidx, bpk);
         }
       }
     }
   }
 }
 
+// (score desc, idx asc) warp argmax carrying the maximiser's packed leaf.
+__device__ __forceinline__ void warp_best_pk(int64_t& s, int64_t& i, int64_t& pk) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const int64_t i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    const int64_t p2 = __shfl_xor_sync(0xffffffffu, pk, o);
+    if (better(s2, i2, s, i)) { s = s2; i = i2; pk = p2; }
+  }
+}
+
 // Greedy (exact pruned) argmax of one state by one warp over the Top lists pwarp_means_top
-// built.  Returns (best, bidx) in all lanes; bidx = INT64_MAX when no action is valid.
+// built.  Returns (best, bidx) and the maximiser's packed leaf bpk (pack_leaf) in all lanes;
+// bidx = INT64_MAX (bpk = -1) when no action is valid.
 __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
                                     const float* __restrict__ z, float meanL, uint64_t sched,
-                                    int64_t& best, int64_t& bidx, int64_t& nevals) {
+                                    int64_t& best, int64_t& bidx, int64_t& bpk, int64_t& nevals) {
   const int lane = threadIdx.x & 31;
   const int W = sp.W;
   (void)sched;
@@ -671,6 +730,7 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
   const int64_t Fv = fixed_point(z[0]);
   best = INT64_MIN;
   bidx = INT64_MAX;
+  bpk = -1;
   // Seed: the search's first-level bound UB(l) = base(l) + sum_k (best Top value of slot k's
   // type) per layout; each lane takes its highest-UB layout (ties: lowest l) and builds that
   // layout's greedy leaf (slot k takes its best Top-list job not already taken -- valid, since
@@ -707,12 +767,12 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
         if (!used) { js[k] = j; v += w.topv[t * 4 + q]; break; }
       }
     }
-    if (C == 1) pleaf<1>(tb, sl, W, js, v, best, bidx);
-    else if (C == 2) pleaf<2>(tb, sl, W, js, v, best, bidx);
-    else if (C == 3) pleaf<3>(tb, sl, W, js, v, best, bidx);
-    else pleaf<4>(tb, sl, W, js, v, best, bidx);
+    if (C == 1) pleaf<1>(tb, sl, W, js, v, best, bidx, bpk);
+    else if (C == 2) pleaf<2>(tb, sl, W, js, v, best, bidx, bpk);
+    else if (C == 3) pleaf<3>(tb, sl, W, js, v, best, bidx, bpk);
+    else pleaf<4>(tb, sl, W, js, v, best, bidx, bpk);
   }
-  warp_best(best, bidx);
+  warp_best_pk(best, bidx, bpk);
   // Exhaustive pruned search, lanes over layouts grouped by slot count (C-uniform rounds).
 #pragma unroll 1
   for (int C = 1; C <= 4; ++C) {
@@ -720,13 +780,13 @@ __device__ inline void pwarp_greedy(const DevSpace& sp, const PTabs& tb, PWarpSm
       const int l = tb.lay_of_c[i];
       const uint32_t ty = tb.stype[l];
       const int64_t base = Fv + fixed_point(z[1 + l] - meanL);
-      if (C == 1) psearch<1>(tb, w, l, W, ty, base, best, bidx, nevals);
-      else if (C == 2) psearch<2>(tb, w, l, W, ty, base, best, bidx, nevals);
-      else if (C == 3) psearch<3>(tb, w, l, W, ty, base, best, bidx, nevals);
-      else psearch<4>(tb, w, l, W, ty, base, best, bidx, nevals);
+      if (C == 1) psearch<1>(tb, w, l, W, ty, base, best, bidx, bpk, nevals);
+      else if (C == 2) psearch<2>(tb, w, l, W, ty, base, best, bidx, bpk, nevals);
+      else if (C == 3) psearch<3>(tb, w, l, W, ty, base, best, bidx, bpk, nevals);
+      else psearch<4>(tb, w, l, W, ty, base, best, bidx, bpk, nevals);
     }
   }
-  warp_best(best, bidx);
+  warp_best_pk(best, bidx, bpk);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -789,17 +849,23 @@ __device__ inline int64_t seq_n_valid(const DevSpace& sp, const PTabs& tb, uint6
 }
 
 template <int X>
+// bpk: the maximiser's packed leaf from the pruned search, -1 from the other argmaxes (their
+// consumers decode the action index).
 __device__ __forceinline__ void greedy(const DevSpace& sp, const PTabs& tb, PWarpSmem& w,
                                        const float* __restrict__ z, float meanL, uint64_t sched,
-                                       int64_t& best, int64_t& bidx, int64_t& nevals) {
+                                       int64_t& best, int64_t& bidx, int64_t& bpk,
+                                       int64_t& nevals) {
+  bpk = -1;
   if (sp.seq) seq_greedy(sp, tb, z, meanL, sched, best, bidx, nevals);
   else if constexpr (X > 0) xgreedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
-  else pwarp_greedy(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+  else pwarp_greedy(sp, tb, w, z, meanL, sched, best, bidx, bpk, nevals);
 }
 
-// k-th valid action (index order), warp-parallel over layouts.
+// k-th valid action (index order), warp-parallel over layouts.  With ol != nullptr also its
+// layout, members in ascending order (og[4]) and permutation rank (ors), in all lanes.
 __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, uint64_t sched,
-                                          int64_t k) {
+                                          int64_t k, int* ol = nullptr, int* og = nullptr,
+                                          int* ors = nullptr) {
   const int lane = threadIdx.x & 31;
   const int W = sp.W;
   const uint64_t all = W == 64 ? ~0ull : ((1ull << W) - 1);
@@ -828,14 +894,22 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
     if (hit) {
       const int src = __ffs(hit) - 1;
       int64_t res = -1;
+      int g[4] = {0, 0, 0, 0}, rsi = 0;
       if (lane == src) {
         const int64_t kk = k - excl;
         const int64_t f = c_fact[C];
         const int64_t rg = kk / f, rs = kk - rg * f;
-        int gp[4], g[4];
+        int gp[4];
         unrank_comb(rg, U, C, gp);
         for (int i = 0; i < C; ++i) g[i] = nth_bit64(freem, gp[i]);
         res = tb.off[l] + rank_comb(g, C, W) * f + rs;
+        rsi = (int)rs;
+      }
+      if (ol) {
+        *ol = __shfl_sync(0xffffffffu, l, src);
+        *ors = __shfl_sync(0xffffffffu, rsi, src);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) og[i] = __shfl_sync(0xffffffffu, g[i], src);
       }
       return __shfl_sync(0xffffffffu, res, src);
     }
@@ -849,26 +923,37 @@ __device__ inline int64_t pwarp_kth_valid(const DevSpace& sp, const PTabs& tb, u
 // and auto-reset (R19).
 __device__ inline void sel_tail(const DevSpace& sp, const DevPool& pool, const PTabs& tb,
                                 const SelArgs& a, int row, const float* z, float meanL,
-                                uint64_t sched, int64_t best, int64_t bidx) {
+                                uint64_t sched, int64_t best, int64_t bidx, int64_t bpk) {
   const int lane = threadIdx.x & 31;
   const int W = sp.W;
   int64_t act = bidx;
+  // the action's layout l, members g (ascending) and their slots sg: from the argmax's packed
+  // leaf, from the k-th valid action's construction, or (other argmaxes) by decoding the index
+  int l = -1, g[4] = {0, 0, 0, 0}, sg[4] = {0, 1, 2, 3};
   if ((uint64_t)a.u_explore[row] < a.thr) {
     const int64_t nv = sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
     const int64_t k = (int64_t)__umul64hi(a.u_action[row], (uint64_t)nv);
-    act = sp.seq ? seq_kth(sp, tb, sched, k) : pwarp_kth_valid(sp, tb, sched, k);
+    if (sp.seq) {
+      act = seq_kth(sp, tb, sched, k);
+    } else {
+      int rs = 0;
+      act = pwarp_kth_valid(sp, tb, sched, k, &l, g, &rs);
+      unlehmer(rs, tb.nsl[l], sg);
+    }
   } else if (bidx == INT64_MAX) {
     // a state always has a valid action, so no maximiser means non-finite Q values (NaN
     // weights): flag it for hrp_sync and keep the environment consistent with the lowest
     // valid action
     if (lane == 0) atomicOr(a.err, 1u);
     act = sp.seq ? seq_kth(sp, tb, sched, 0) : pwarp_kth_valid(sp, tb, sched, 0);
+  } else if (bpk >= 0) {
+    int t4[4];
+    l = leaf_members(tb, bpk, g, sg, t4);
   }
+  if (l < 0) l = decode_action(sp, act, g, sg);   // every lane (same result)
   const uint8_t* wr = a.win + (size_t)row * W;
   int64_t slot = 0;
   int d = 0;
-  int g[4], sg[4];
-  const int l = decode_action(sp, act, g, sg);   // every lane (same result)
   const int C = tb.nsl[l];
   const uint32_t ty = tb.stype[l];
   // slot-type means of the action's members (sel_kernel's, written per row), for Q of an
@@ -923,6 +1008,12 @@ __device__ inline void sel_tail(const DevSpace& sp, const DevPool& pool, const P
   }
   slot = __shfl_sync(0xffffffffu, slot, 0);
   d = __shfl_sync(0xffffffffu, d, 0);
+  {   // the transition's action descriptor (read back by the update's sampler for tdq)
+    int t4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) t4[i] = (ty >> (8 * sg[i])) & 255;
+    desc_from_members(sp, l, C, g, t4, a.rep_desc + (size_t)slot * 8);
+  }
   uint8_t* wm = a.win + (size_t)row * W;
   for (int j = lane; j < W; j += 32) a.rep_win[slot * W + j] = wm[j];
   __syncwarp();
@@ -950,8 +1041,8 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
       __syncwarp();
       for (int t = lane; t < sp.T; t += 32) a.g_meanJ[(size_t)row * sp.T + t] = w.meanJ[t];
     }
-    int64_t best, bidx;
-    greedy<X>(sp, tb, w, z, meanL, sched, best, bidx, nevals);
+    int64_t best, bidx, bpk;
+    greedy<X>(sp, tb, w, z, meanL, sched, best, bidx, bpk, nevals);
     ncovered += sp.seq ? seq_n_valid(sp, tb, sched) : n_valid(sp, sched);
     if (lane == 0) {
       if (a.mode == SEL_INFER) {
@@ -961,6 +1052,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
       } else {   // the rest of a5-a7: sel_tail_kernel
         a.g_best[row] = best;
         a.g_bidx[row] = bidx;
+        a.g_pk[row] = bpk;
         a.g_meanL[row] = meanL;
       }
     }
@@ -984,7 +1076,7 @@ __global__ void __launch_bounds__(256) sel_tail_kernel(DevSpace sp, DevPool pool
   tg.stype = const_cast<uint32_t*>(sp.lay_stype);
   tg.nsl = const_cast<uint8_t*>(sp.lay_n);
   sel_tail(sp, pool, tg, a, row, a.z + (size_t)row * sp.H, a.g_meanL[row], a.sched[row],
-           a.g_best[row], a.g_bidx[row]);
+           a.g_best[row], a.g_bidx[row], a.g_pk[row]);
 }
 
 // Action idx -> layout, members g_i and their slot types t_i (returns l; C = nsl[l]).
@@ -1052,7 +1144,7 @@ __device__ inline float pwarp_qdesc(const int* __restrict__ d, const float* __re
 // (y = r when done), delta = Q(s, a) - y; dsq = delta^2, hdesc word 0 = delta / (B world).  The
 // last block to finish (ticket counter, reset by that block) reduces the loss = sum dsq / (2B)
 // exactly as loss_kernel does (256 threads, strided partial sums, block tree): same bits.
-__global__ void __launch_bounds__(256) tdq_kernel(DevSpace sp, TdArgs a) {
+__global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
   __shared__ float red[32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31;
@@ -1060,18 +1152,6 @@ __global__ void __launch_bounds__(256) tdq_kernel(DevSpace sp, TdArgs a) {
   if (b < a.B) {
     const int* td = a.tdesc + (size_t)b * 8;
     int* hd = a.hdesc + (size_t)b * 8;
-    {   // action descriptors of a (hdesc, also read by the head backward) and a* (tdesc)
-      PTabs tg{};
-      tg.stype = const_cast<uint32_t*>(sp.lay_stype);
-      tg.nsl = const_cast<uint8_t*>(sp.lay_n);
-      write_desc(sp, tg, a.bact[b], hd);
-      if (a.bdone[b] != 0) {
-        if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
-      } else {
-        write_desc(sp, tg, a.astar[b], a.tdesc + (size_t)b * 8);
-      }
-      __syncwarp();
-    }
     float y = a.br[b];
     if (td[2] >= 0)   // -1: done (no bootstrap); 0 job rows in the flat head
       y += a.gamma * pwarp_qdesc(td, a.ht_hi + (size_t)b * a.w, a.ht_lo + (size_t)b * a.w, a.Wt,
@@ -1117,7 +1197,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 :
   int64_t nevals = 0, ncovered = 0;
   for (int b = next_row(a.ctr, a.B, nw); b < a.B; b = next_row(a.ctr, a.B, nw)) {
     const bool done = a.bdone[b] != 0;
-    int64_t astar = -1;
+    int64_t astar = -1, apk = -1;
     // the argmax a* on s' here; both Q values, delta and the loss terms in tdq_kernel from the
     // action descriptors (tdesc: a*, hdesc: a)
     if (!done) {
@@ -1126,7 +1206,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 :
                               ? pwarp_means_top<X == 0 ? 1 : 4>(sp, zn, a.bsched[a.B + b], w)
                               : pwarp_means(sp, zn, w.meanJ);
       int64_t best;
-      greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, nevals);
+      greedy<X>(sp, tb, w, zn, meanL, a.bsched[a.B + b], best, astar, apk, nevals);
       ncovered += sp.seq ? seq_n_valid(sp, tb, a.bsched[a.B + b]) : n_valid(sp, a.bsched[a.B + b]);
       if (astar == INT64_MAX) {   // non-finite Q (see sel_kernel): flag, lowest valid action
         if (lane == 0) atomicOr(a.err, 1u);
@@ -1134,7 +1214,17 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 :
                        : pwarp_kth_valid(sp, tb, a.bsched[a.B + b], 0);
       }
     }
-    if (lane == 0) a.astar[b] = astar;   // -1 when done; descriptors: tdq_kernel
+    if (lane == 0 && a.astar) a.astar[b] = astar;
+    // a*'s descriptor for tdq_kernel (a's descriptor comes from the replay ring via the sampler)
+    if (done) {
+      if (lane == 2) a.tdesc[(size_t)b * 8 + 2] = -1;
+    } else if (apk >= 0) {
+      int g[4], sg[4], t4[4];
+      const int l = leaf_members(tb, apk, g, sg, t4);
+      desc_from_members(sp, l, tb.nsl[l], g, t4, a.tdesc + (size_t)b * 8);
+    } else {
+      write_desc(sp, tb, astar, a.tdesc + (size_t)b * 8);
+    }
     __syncwarp();
   }
   if (a.n_evals) {
