@@ -77,6 +77,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// 2D tensor store of a (32 columns x 32 rows) SWIZZLE_128B box from shared memory (bulk group).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
 // K-major operand tile of `rows` x (4 BKT) B: BKT = 32 fp32 per row in SWIZZLE_128B layout
 // (8-row atoms of 1024 B), BKT = 16 in SWIZZLE_64B (8-row atoms of 512 B).
 template <int BKT>
@@ -159,6 +169,8 @@ struct TcArgs {
   // summed in fp32 in the epilogue.  tmem_cols = the power-of-two allocation.
   int nmain, ncorr, tmem_cols;
   int fast;                // 1: one TF32 MMA per K step (hi . hi), lo planes not loaded
+  int tma_d;               // 1: D (and Dlo) are written by TMA stores from shared memory (maps
+                           //    mapD0 / mapD1; dense rows, ldd % 4 == 0, no split-K)
   unsigned long long* trace;  // diagnostics: per-event timestamps of CTA (0,0,0), or null
 };
 
@@ -192,6 +204,7 @@ template <int BN, int STAGES, int EPI, int BKT = BK>
 __global__ void __launch_bounds__(kThreadsTc, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                const __grid_constant__ CUtensorMap mapB0, const __grid_constant__ CUtensorMap mapB1,
+               const __grid_constant__ CUtensorMap mapD0, const __grid_constant__ CUtensorMap mapD1,
                const TcArgs a) {
   using S = TcSmem<BN, STAGES, BKT>;
   extern __shared__ uint8_t smem_raw[];
@@ -319,6 +332,96 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
     asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x == 128) TRACE(194);
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
+    if (EPI != TC_EPI_STORE && a.tma_d) {
+      // lane <-> row rbase + lane with the chunk's 32 columns in registers: bias / ReLU / mask per
+      // element, D (hi, lo) staged in a per-warp 32 x 128 B SWIZZLE_128B box and written by TMA
+      // stores (asynchronous bulk writes, the box clipped at M and N), D^T written directly
+      // (lanes = consecutive rows: coalesced)
+      const bool dsplit = a.Dlo != nullptr, tsplit = a.DTlo != nullptr;
+      uint8_t* tb = smem + 36864 + warp * 8192;   // after the 8 x 32 x 33 tiles; 1024-B aligned
+      const int row = rbase + lane;
+      const bool rv = row < a.M;
+#pragma unroll 1
+      for (int u = 0; u < (NCH + 1) / 2; ++u) {
+        const int q = 2 * u + wh;
+        if (q >= NCH) break;                     // warp-uniform
+        const int c = q * 32;
+        if (n0 + c >= a.N) break;                // warp-uniform
+        uint32_t v[32];
+        TMEM_LD32(trow + c, v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        {
+          const int nm = min(a.nmain, nk);
+          for (int q2 = 1; q2 < nm + a.ncorr; ++q2) {
+            const int slot = q2 < nm ? q2 : a.nmain;
+            uint32_t w2[32];
+            TMEM_LD32(trow + (uint32_t)(slot * BN) + c, w2);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w2[j]));
+          }
+        }
+        const int col0 = n0 + c;
+        float x[32];
+        if (EPI == TC_EPI_RELU_MASK) {           // the row's 32 mask values, 16-byte loads
+          const float* mp = a.aux + (size_t)row * a.ldaux + col0;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (rv && col0 + 4 * j4 < a.N) m4 = *reinterpret_cast<const float4*>(mp + 4 * j4);
+            x[4 * j4 + 0] = m4.x > 0.f ? __uint_as_float(v[4 * j4 + 0]) : 0.f;
+            x[4 * j4 + 1] = m4.y > 0.f ? __uint_as_float(v[4 * j4 + 1]) : 0.f;
+            x[4 * j4 + 2] = m4.z > 0.f ? __uint_as_float(v[4 * j4 + 2]) : 0.f;
+            x[4 * j4 + 3] = m4.w > 0.f ? __uint_as_float(v[4 * j4 + 3]) : 0.f;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float y = __uint_as_float(v[j]);
+            if (EPI == TC_EPI_BIAS || EPI == TC_EPI_BIAS_RELU) y += col0 + j < a.N ? a.bias[col0 + j] : 0.f;
+            if (EPI == TC_EPI_BIAS_RELU) y = fmaxf(y, 0.f);
+            x[j] = y;
+          }
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();                            // the staging box is free again
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float4 h4, l4;
+          float* hp = &h4.x;
+          float* lp = &l4.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float xv = x[4 * k + e];
+            const float h = dsplit ? tf32_rna(xv) : xv;
+            hp[e] = h;
+            lp[e] = xv - h;
+          }
+          const int off = lane * 128 + ((k ^ (lane & 7)) << 4);
+          *reinterpret_cast<float4*>(tb + off) = h4;
+          if (dsplit) *reinterpret_cast<float4*>(tb + 4096 + off) = l4;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&mapD0, tb, col0, rbase);
+          if (dsplit) tma_store_2d(&mapD1, tb + 4096, col0, rbase);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (a.DT != nullptr && rbase < a.t_rows && rv && row < a.t_rows) {
+          const ptrdiff_t dtlo = tsplit ? a.DTlo - a.DT : 0;
+#pragma unroll 8
+          for (int j = 0; j < 32; ++j) {
+            if (col0 + j < a.N) {
+              float* tp = a.DT + (size_t)(col0 + j) * a.ldt + row;
+              store_split(tp, tsplit ? tp + dtlo : nullptr, x[j]);
+            }
+          }
+        }
+      }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      __syncwarp();
+    } else {
     // the stage buffers are idle now: per-warp 32 x 33 transpose tile
     float* stg = reinterpret_cast<float*>(smem) + warp * (32 * 33);
     float* Dz = a.D + (size_t)blockIdx.z * a.M * a.ldd;
@@ -384,6 +487,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant_
         }
       }
       __syncwarp();
+    }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -550,6 +654,8 @@ bool make_map(CUtensorMap* m, const float* p, int rows, int cols, int ld, int bo
 }
 
 int g_acc_mode = 2;   // 0: one accumulator; 1: main + correction; 2: up to 3 mains + correction
+// D written through TMA stores when its layout allows (HRP_NO_TMA_STORE=1: generic stores, A/B)
+static const bool g_tma_store = std::getenv("HRP_NO_TMA_STORE") == nullptr;
 
 template <int BN, int STAGES, int EPI, int BKT = BK>
 hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
@@ -565,6 +671,16 @@ hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   // boxes never exceed the tensor; rows of a tile beyond the box only feed masked outputs
   a.boxA = std::min(BM, a.M);
   a.boxB = std::min(BN, a.N);
+  CUtensorMap md0, md1;
+  a.tma_d = 0;
+  if (EPI != TC_EPI_STORE && g_tma_store && splits == 1 && a.D != nullptr && a.ldd % 4 == 0 &&
+      ((uintptr_t)a.D & 15) == 0 && (a.Dlo == nullptr || ((uintptr_t)a.Dlo & 15) == 0)) {
+    if (!make_map(&md0, a.D, a.M, a.N, a.ldd, 32) ||
+        (a.Dlo != nullptr && !make_map(&md1, a.Dlo, a.M, a.N, a.ldd, 32)))
+      return HRP_ECUDA;
+    if (a.Dlo == nullptr) md1 = md0;
+    a.tma_d = 1;
+  }
   if (!make_map(&ma0, A.hi, a.M, a.K, a.lda, a.boxA, BKT) ||
       !make_map(&ma1, A.lo, a.M, a.K, a.lda, a.boxA, BKT) ||
       !make_map(&mb0, B.hi, a.N, a.K, a.ldb, a.boxB, BKT) ||
@@ -592,7 +708,9 @@ hrp_status launch(cudaStream_t st, Planes A, Planes B, TcArgs a, int splits) {
   at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES, EPI, BKT>, ma0, ma1, mb0, mb1, a);
+  if (!a.tma_d) { md0 = ma0; md1 = ma0; }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, STAGES, EPI, BKT>, ma0, ma1, mb0, mb1,
+                                     md0, md1, a);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { g_tc_err = cudaGetErrorString(e); return HRP_ECUDA; }
   return HRP_OK;
