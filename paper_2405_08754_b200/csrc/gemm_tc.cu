@@ -766,7 +766,7 @@ static hrp_status run_bn(int bn, cudaStream_t st, Planes A, Planes B, const TcAr
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, Planes A,
                        int lda, Planes B, int ldb, const float* bias, const float* aux, int ldaux,
                        float* D, float* Dlo, float* DT, float* DTlo, int t_rows,
-                       unsigned long long* trace, int fast) {
+                       unsigned long long* trace, int fast, int ldd) {
   g->launches++;
   TcArgs a{};
   a.fast = fast;
@@ -774,7 +774,7 @@ hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K,
   a.M = M; a.N = N; a.K = K; a.kc = K;
   a.lda = lda; a.ldb = ldb;
   a.bias = bias; a.aux = aux; a.ldaux = ldaux;
-  a.D = D; a.Dlo = Dlo; a.ldd = N;
+  a.D = D; a.Dlo = Dlo; a.ldd = ldd > 0 ? ldd : N;
   a.DT = DT; a.DTlo = DT ? DTlo : nullptr; a.ldt = (t_rows + 3) / 4 * 4; a.t_rows = DT ? t_rows : 0;
   const int bn = pick_bn(M, N, K, g->nsm);
   if (epi == TC_EPI_BIAS) return run_bn<TC_EPI_BIAS>(bn, st, A, B, a);

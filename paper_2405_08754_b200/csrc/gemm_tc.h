@@ -22,11 +22,11 @@ inline int r4(int x) { return (x + 3) / 4 * 4; }
 // aux [M][ldaux] (ReLU mask source: x > 0 iff its hi plane > 0); DT optional [N][t_rows]
 // transposed copy of D's first t_rows rows (split into (DT, DTlo) when DTlo != NULL).
 // Row strides lda / ldb are in elements and must be multiples of 4 (TMA); D^T has row stride
-// round_up(t_rows, 4).
+// round_up(t_rows, 4).  ldd: D's row stride (0: N).
 hrp_status tc_gemm_run(TcGemm* g, cudaStream_t st, int epi, int M, int N, int K, Planes A,
                        int lda, Planes B, int ldb, const float* bias, const float* aux, int ldaux,
                        float* D, float* Dlo, float* DT, float* DTlo, int t_rows,
-                       unsigned long long* trace = nullptr, int fast = 0);
+                       unsigned long long* trace = nullptr, int fast = 0, int ldd = 0);
 // Weight gradient: D[M][N] = A[M][K] . B[N][K]^T (K % 4 == 0, dense rows), split-K over K with
 // a deterministic reduction through ws (>= S * M * N floats).  With db != NULL the last row of
 // B is a ones row (hi 1, lo 0): column N-1 of the product is the row sum of A (the bias

@@ -270,6 +270,7 @@ struct hrp_ctx {
   int64_t t = 0, inserted = 0;
   // workspaces
   int rows_max = 0;
+  int ldz = 0;                        // row stride of z: round_up(H, 4) (TMA-storable rows)
   Pl X;                               // [rows][in]
   std::vector<Pl> act;                // hidden outputs [rows][w] per layer
   float* z = nullptr;                 // [rows][H]
@@ -430,11 +431,11 @@ hrp_status split_weights(hrp_ctx* c, bool target) {
 // the first t_rows rows of D.
 hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, Planes A, int lda,
                   const float* Bh, const float* Bl, const float* bias, const float* aux, int ldaux,
-                  Pl D, Pl DT = Pl{}, int t_rows = 0) {
+                  Pl D, Pl DT = Pl{}, int t_rows = 0, int ldd = 0) {
   prof_begin(c);
   hrp_status s = tc_gemm_run(c->tc, c->stream, epi, M, N, K, A, lda, Planes{Bh, Bl}, r4(K), bias,
                              aux, ldaux, D.hi, D.lo, DT.hi, DT.lo, t_rows, nullptr,
-                             c->cfg.precision == 1);
+                             c->cfg.precision == 1, ldd);
   if (s) return fail(s, tc_gemm_error());
   c->launches += tc_gemm_launches(c->tc) - 1;
   return launch_check(c, cls);
@@ -458,7 +459,8 @@ hrp_status transpose(hrp_ctx* c, int cls, int rows, int cols, int ld_src, Pl src
 // offsets in z_out); head_from >= M skips it (the structured update needs the head only where
 // every action is scored).
 hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out,
-                       int t_rows = 0, const std::vector<Pl>* acts = nullptr, int head_from = 0) {
+                       int t_rows = 0, const std::vector<Pl>* acts = nullptr, int head_from = 0,
+                       int ldz = 0) {
   const std::vector<Pl>& act = acts ? *acts : c->act;
   c->gemm_cls = HRP_K_GEMM_FWD;
   const int nl = (int)c->dims.size() - 1;
@@ -475,12 +477,14 @@ hrp_status mlp_forward(hrp_ctx* c, const float* theta, Pl X, int M, float* z_out
       const Pl hs = h.off((size_t)head_from * ldh);
       const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
       return tc_run(c, HRP_K_GEMM_FWD, TC_EPI_BIAS, M - head_from, fo, fi, hs.c(), ldh, hi,
-                    hi + c->sstride, b, nullptr, 0, Pl{z_out + (size_t)head_from * fo, nullptr});
+                    hi + c->sstride, b, nullptr, 0,
+                    Pl{z_out + (size_t)head_from * (ldz > 0 ? ldz : fo), nullptr}, Pl{}, 0, ldz);
     }
     const Pl outT = (i < nl - 1 && t_rows > 0) ? c->actT[i] : Pl{};
     const float* hi = c->wsplit + (target ? 2 : 0) * c->sstride + c->soff[i];
     s = tc_run(c, HRP_K_GEMM_FWD, i < nl - 1 ? TC_EPI_BIAS_RELU : TC_EPI_BIAS, M, fo, fi, h.c(),
-               ldh, hi, hi + c->sstride, b, nullptr, 0, out, outT, t_rows);
+               ldh, hi, hi + c->sstride, b, nullptr, 0, out, outT, t_rows,
+               i == nl - 1 ? ldz : 0);
     if (s) return s;
     h = out;
     ldh = fo;
@@ -826,7 +830,8 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(alloc_pl(c->X, R * c->ldX, true));
   c->act.resize(cfg->hidden_layers);
   for (auto& p : c->act) CK(alloc_pl(p, R * wd, true));
-  CK(ar.alloc((void**)&c->z, sizeof(float) * R * H));
+  c->ldz = r4(H);
+  CK(ar.alloc((void**)&c->z, sizeof(float) * R * c->ldz));
   c->act_t.resize(cfg->hidden_layers);
   for (auto& p : c->act_t) CK(alloc_pl(p, (size_t)B * wd, true));
   {
@@ -966,10 +971,11 @@ hrp_status hrp_env_step(hrp_ctx* c, uint64_t thr, const uint32_t* d_u_explore,
   encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool, c->X.hi,
                                                      c->X.lo, c->ldX);
   if ((s = launch_check(c, HRP_K_ENCODE))) return s;
-  if ((s = mlp_forward(c, c->theta, c->X, E, c->z))) return s;
+  if ((s = mlp_forward(c, c->theta, c->X, E, c->z, 0, nullptr, 0, c->ldz))) return s;
   SelArgs a{};
   a.M = E;
   a.z = c->z;
+  a.ldz = c->ldz;
   a.mode = SEL_STEP;
   a.win = c->win;
   a.sched = c->sched;
@@ -1013,10 +1019,12 @@ hrp_status hrp_q_forward(hrp_ctx* c, int64_t n, const uint8_t* d_windows, const 
                                                        c->ldX);
     if ((s = launch_check(c, HRP_K_ENCODE))) return s;
     float* zo = d_head ? d_head + r0 * H : c->z;
-    if ((s = mlp_forward(c, c->theta, c->X, M, zo))) return s;
+    const int ldz = d_head ? H : c->ldz;     // the caller's head rows are dense
+    if ((s = mlp_forward(c, c->theta, c->X, M, zo, 0, nullptr, 0, ldz))) return s;
     SelArgs a{};
     a.M = M;
     a.z = zo;
+    a.ldz = ldz;
     a.mode = SEL_INFER;
     a.win = const_cast<uint8_t*>(wp);
     a.sched = const_cast<uint64_t*>(sp);
@@ -1076,7 +1084,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   if (conc) {
     if ((s = on_side(c, target_pass))) return s;
   }
-  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, B, nullptr, B))) return s;
+  if ((s = mlp_forward(c, c->theta, c->X, 2 * B, c->z, B, nullptr, B, c->ldz))) return s;
   if (conc) {
     if ((s = join(c))) return s;
   } else if ((s = target_pass())) {
@@ -1085,6 +1093,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   TdArgs t{};
   t.B = B;
   t.z_all = c->z;
+  t.ldz = c->ldz;
   t.bsched = c->bsched;
   t.bact = c->bact;
   t.br = c->br;

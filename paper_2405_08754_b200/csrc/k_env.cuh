@@ -184,7 +184,8 @@ enum SelMode { SEL_STEP = 0, SEL_INFER = 1 };
 
 struct SelArgs {
   int M;                    // rows
-  const float* z;           // [M][H]
+  const float* z;           // [M][ldz] head rows (H used)
+  int ldz;
   int mode;                 // SelMode
   bool explicit_mode;
   // state
@@ -288,7 +289,8 @@ sample_encode_kernel(DevSpace sp, DevPool pool, int B, const uint32_t* __restric
 
 struct TdArgs {
   int B;
-  const float* z_all;   // [2B][H]: rows [B,2B) online(s') (rows [0,B) are not computed)
+  const float* z_all;   // [2B][ldz]: rows [B,2B) online(s') (rows [0,B) are not computed)
+  int ldz;
   const uint64_t* bsched;  // [2B]
   const int64_t* bact;
   const float* br;

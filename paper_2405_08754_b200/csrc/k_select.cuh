@@ -1032,7 +1032,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   const int nw = gridDim.x * pwarps(X > 0);
   int64_t nevals = 0, ncovered = 0;
   for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
-    const float* zg = a.z + (size_t)row * sp.H;
+    const float* zg = a.z + (size_t)row * a.ldz;
     const float* z = zg;
     const uint64_t sched = a.sched[row];
     const float meanL = (X <= 0 && !sp.seq) ? pwarp_means_top<X == 0 ? 1 : 4>(sp, z, sched, w)
@@ -1075,7 +1075,7 @@ __global__ void __launch_bounds__(256) sel_tail_kernel(DevSpace sp, DevPool pool
   tg.off = const_cast<int64_t*>(sp.off);
   tg.stype = const_cast<uint32_t*>(sp.lay_stype);
   tg.nsl = const_cast<uint8_t*>(sp.lay_n);
-  sel_tail(sp, pool, tg, a, row, a.z + (size_t)row * sp.H, a.g_meanL[row], a.sched[row],
+  sel_tail(sp, pool, tg, a, row, a.z + (size_t)row * a.ldz, a.g_meanL[row], a.sched[row],
            a.g_best[row], a.g_bidx[row], a.g_pk[row]);
 }
 
@@ -1201,7 +1201,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 :
     // the argmax a* on s' here; both Q values, delta and the loss terms in tdq_kernel from the
     // action descriptors (tdesc: a*, hdesc: a)
     if (!done) {
-      const float* zn = a.z_all + (size_t)(a.B + b) * sp.H;
+      const float* zn = a.z_all + (size_t)(a.B + b) * a.ldz;
       const float meanL = (X <= 0 && !sp.seq)
                               ? pwarp_means_top<X == 0 ? 1 : 4>(sp, zn, a.bsched[a.B + b], w)
                               : pwarp_means(sp, zn, w.meanJ);
