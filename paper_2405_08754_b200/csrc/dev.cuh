@@ -24,6 +24,7 @@ struct DevSpace {
   const uint64_t* combo_mask[5];
   int ncombo[5];
   int nlay_c[5];               // layouts with C slots
+  const uint16_t* lay_of_c;    // [L] layouts grouped by slot count (C ascending, index order)
   int64_t n_actions;
 };
 

@@ -167,6 +167,13 @@ hrp_status upload_tables(const HostSpace& hs, const hrp_profiles* prof, bool com
     d.nlay_c[C] = 0;
   }
   for (int l = 0; l < L; ++l) d.nlay_c[hs.nslots[l]]++;
+  {
+    std::vector<uint16_t> byc;
+    for (int C = 1; C <= 4; ++C)
+      for (int l = 0; l < L; ++l)
+        if (hs.nslots[l] == C) byc.push_back((uint16_t)l);
+    CK(upload(ar, (uint16_t**)&d.lay_of_c, byc.data(), byc.size(), st));
+  }
   if (combos) {
     for (int C = 1; C <= hs.cmax; ++C) {
       std::vector<uint32_t> mem;

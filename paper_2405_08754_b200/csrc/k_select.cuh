@@ -127,6 +127,7 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
   for (int i = threadIdx.x; i < sp.L; i += blockDim.x) {
     t.stype[i] = sp.lay_stype[i];
     t.nsl[i] = sp.lay_n[i];
+    t.lay_of_c[i] = sp.lay_of_c[i];   // host-built grouping (layouts by slot count)
   }
   int k = 0;
   for (int C = 1; C <= 4; ++C) {
@@ -135,13 +136,6 @@ __device__ inline PTabs pload_tabs(const DevSpace& sp, uint8_t* base, PWarpSmem&
   }
   t.cstart[0] = 0;
   t.cstart[5] = k;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int q = 0;
-    for (int C = 1; C <= 4; ++C)
-      for (int l = 0; l < sp.L; ++l)
-        if (t.nsl[l] == C) t.lay_of_c[q++] = (uint16_t)l;
-  }
   __syncthreads();
   return t;
 }
