@@ -612,7 +612,9 @@ hrp_status launch_select(hrp_ctx* c, SelArgs& a) {
   a.explicit_mode = c->explicit_mode;
   a.err = c->dev_err;
   a.n_evals = c->n_evals;
-  a.ctr = c->sched_ctr;
+  // few rows per warp (cfg 2: ~1.7): static assignment, no scheduler atomics; many (cfg 4:
+  // ~28): the dynamic scheduler balances the per-state search cost
+  a.ctr = (int64_t)a.M > 4 * (int64_t)c->p_grid * pwarps(c->explicit_mode) ? c->sched_ctr : nullptr;
   prof_begin(c);
   const int rpc = sel_rows_per_cta(c->explicit_mode);
   const int grid = std::min((a.M + rpc - 1) / rpc, c->p_grid);
@@ -1126,7 +1128,7 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   t.dsq = c->dsq;
   t.astar = d_astar;
   t.n_evals = c->n_evals + 1;
-  t.ctr = c->sched_ctr + 1;
+  t.ctr = (int64_t)B > 4 * (int64_t)c->p_grid * pwarps(c->explicit_mode) ? c->sched_ctr + 1 : nullptr;
   t.err = c->dev_err;
   prof_begin(c);
   {

@@ -273,8 +273,18 @@ __device__ inline float pwarp_means_top(const DevSpace& sp, const float* __restr
   return meanL;
 }
 
-// Dynamic row scheduler: rows are handed out one at a time to warps; the counter wraps back
-// to 0 after the last warp's final (failing) fetch, so it needs no reset between launches.
+// Row scheduler.  ctr == nullptr: static, warp g takes rows g, g + nwarps, ... (cur = the row it
+// just finished, -1 to start).  Otherwise dynamic: rows are handed out one at a time to warps;
+// the counter wraps back to 0 after the last warp's final (failing) fetch, so it needs no reset
+// between launches.
+__device__ __forceinline__ int next_row_s(unsigned* ctr, int M, int nwarps, int cur) {
+  if (ctr == nullptr)
+    return cur < 0 ? (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) : cur + nwarps;
+  unsigned r = 0;
+  if ((threadIdx.x & 31) == 0) r = atomicInc(ctr, (unsigned)(M + nwarps - 1));
+  return (int)__shfl_sync(0xffffffffu, r, 0);
+}
+
 __device__ __forceinline__ int next_row(unsigned* ctr, int M, int nwarps) {
   unsigned r = 0;
   if ((threadIdx.x & 31) == 0) r = atomicInc(ctr, (unsigned)(M + nwarps - 1));
@@ -1025,7 +1035,7 @@ sel_kernel(DevSpace sp, DevPool pool, SelArgs a) {
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * pwarps(X > 0);
   int64_t nevals = 0, ncovered = 0;
-  for (int row = next_row(a.ctr, a.M, nw); row < a.M; row = next_row(a.ctr, a.M, nw)) {
+  for (int row = next_row_s(a.ctr, a.M, nw, -1); row < a.M; row = next_row_s(a.ctr, a.M, nw, row)) {
     const float* zg = a.z + (size_t)row * a.ldz;
     const float* z = zg;
     const uint64_t sched = a.sched[row];
@@ -1189,7 +1199,7 @@ __global__ void __launch_bounds__(pwarps(X > 0) * 32, X <= 0 ? 2 : (X == 4 ? 3 :
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * pwarps(X > 0);
   int64_t nevals = 0, ncovered = 0;
-  for (int b = next_row(a.ctr, a.B, nw); b < a.B; b = next_row(a.ctr, a.B, nw)) {
+  for (int b = next_row_s(a.ctr, a.B, nw, -1); b < a.B; b = next_row_s(a.ctr, a.B, nw, b)) {
     const bool done = a.bdone[b] != 0;
     int64_t astar = -1, apk = -1;
     // the argmax a* on s' here; both Q values, delta and the loss terms in tdq_kernel from the
