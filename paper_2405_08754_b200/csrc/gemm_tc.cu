@@ -746,7 +746,8 @@ static int pick_bn(int M, int N, int K, int nsm) {
   // (fewer operand re-reads from L2).
   const long mt = (M + BM - 1) / BM;
   const long t64 = mt * ((N + 63) / 64), t128 = mt * ((N + 127) / 128), t256 = mt * ((N + 255) / 256);
-  if (t64 > 4L * nsm) return K <= 512 ? 256 : 128;
+  if (t64 > 4L * nsm) return 256;   // 4-stage BK16 256-wide tiles: best at every K measured
+                                    // (cfg4 K = 1088: 12.79 -> 12.64 ms/step vs 128-wide)
   const double T256 = K <= 256 ? 2.3 : (K <= 512 ? 2.8 : 3.0);
   const double c64 = (double)((t64 + nsm - 1) / nsm);
   const double c128 = 1.31 * (double)((t128 + nsm - 1) / nsm);
