@@ -741,9 +741,9 @@ static const bool g_bk16 = !std::getenv("HRP_BK32");
 static int pick_bn(int M, int N, int K, int nsm) {
   if (g_force_bn == 64 || g_force_bn == 128 || g_force_bn == 256) return g_force_bn;
   // Cost model from the measured per-CTA times (profiles/diag_gemm.py, one CTA per SM):
-  // relative CTA time 1.0 / 1.31 / T256 for BN = 64 / 128 / 256 (BN = 256 runs 2 stages, so it
-  // slows down with K), times the number of waves; many-wave problems prefer the wide tiles
-  // (fewer operand re-reads from L2).
+  // relative CTA time 1.0 / 1.31 / T256 for BN = 64 / 128 / 256 (measured with the 2-stage
+  // 256-wide tiles; the 4-stage BK16 ones are no slower), times the number of waves; many-wave
+  // problems take the wide tiles (fewer operand re-reads from L2).
   const long mt = (M + BM - 1) / BM;
   const long t64 = mt * ((N + 63) / 64), t128 = mt * ((N + 127) / 128), t256 = mt * ((N + 255) / 256);
   if (t64 > 4L * nsm) return 256;   // 4-stage BK16 256-wide tiles: best at every K measured
