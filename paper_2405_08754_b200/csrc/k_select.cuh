@@ -1147,7 +1147,7 @@ __device__ inline float pwarp_qdesc(const int* __restrict__ d, const float* __re
 // Structured-mode tail of the TD step (a9-a10): warp per sample, y = r + gamma Q_target(s', a*)
 // (y = r when done), delta = Q(s, a) - y; dsq = delta^2, hdesc word 0 = delta / (B world).  The
 // last block to finish (ticket counter, reset by that block) reduces the loss = sum dsq / (2B)
-// exactly as loss_kernel does (256 threads, strided partial sums, block tree): same bits.
+// from the blocks' partial sums (each block's samples in order), a fixed order: deterministic.
 __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
   __shared__ float red[32];
   __shared__ bool last;
@@ -1175,6 +1175,13 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
     }
   }
   if (a.loss == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {   // the block's partial sum, its samples in order (fixed order)
+    const int b0 = blockIdx.x * (blockDim.x >> 5);
+    float p = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5) && b0 + i < a.B; ++i) p += a.dsq[b0 + i];
+    a.dsq[a.B + blockIdx.x] = p;   // dsq holds >= 2B floats
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1185,8 +1192,9 @@ __global__ void __launch_bounds__(256) tdq_kernel(TdArgs a) {
   __syncthreads();
   if (!last) return;
   __threadfence();
-  float acc = 0.f;
-  for (int i = threadIdx.x; i < a.B; i += blockDim.x) acc += ((volatile const float*)a.dsq)[i];
+  float acc = 0.f;   // the blocks' partials (B / 8 values instead of B), fixed order
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x)
+    acc += ((volatile const float*)a.dsq)[a.B + i];
   acc = block_sum(acc, red);
   if (threadIdx.x == 0) *a.loss = acc / (2.f * (float)a.B);
 }
