@@ -448,15 +448,6 @@ hrp_status tc_run(hrp_ctx* c, int cls, int epi, int M, int N, int K, Planes A, i
   return launch_check(c, cls);
 }
 
-// Transposed copy dst [cols][ld_dst] of both planes of src [rows][cols] (ld_src).
-hrp_status transpose(hrp_ctx* c, int cls, int rows, int cols, int ld_src, Pl src, Pl dst,
-                     int ld_dst) {
-  prof_begin(c);
-  hrp_status s = tc_transpose(c->tc, c->stream, rows, cols, ld_src, src.c(), ld_dst, dst.hi, dst.lo);
-  if (s) return fail(s, tc_gemm_error());
-  c->launches += tc_gemm_launches(c->tc) - 1;
-  return launch_check(c, cls);
-}
 
 // Forward of one network over M rows of X: hidden outputs to c->act (kept for the backward
 // pass), head output z_out [M][H] (raw).  With t_rows > 0 the first t_rows rows of every hidden

@@ -285,11 +285,6 @@ __device__ __forceinline__ int next_row_s(unsigned* ctr, int M, int nwarps, int 
   return (int)__shfl_sync(0xffffffffu, r, 0);
 }
 
-__device__ __forceinline__ int next_row(unsigned* ctr, int M, int nwarps) {
-  unsigned r = 0;
-  if ((threadIdx.x & 31) == 0) r = atomicInc(ctr, (unsigned)(M + nwarps - 1));
-  return (int)__shfl_sync(0xffffffffu, r, 0);
-}
 
 // F(cJ[j][tau]) from global z
 __device__ __forceinline__ int64_t Fj(const DevSpace& sp, const float* z, const float* meanJ, int j,
