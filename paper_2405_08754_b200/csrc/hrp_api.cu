@@ -279,6 +279,8 @@ struct hrp_ctx {
   int rows_max = 0;
   int ldz = 0;                        // row stride of z: round_up(H, 4) (TMA-storable rows)
   Pl X;                               // [rows][in]
+  Pl Xenv;                            // [E][in]: the environments' current states, encoded
+  bool xenv_valid = false;            //   by the last update for the next env step
   std::vector<Pl> act;                // hidden outputs [rows][w] per layer
   float* z = nullptr;                 // [rows][H]
   std::vector<Pl> dhs, dhTs;          // backward: per hidden layer dH, dH^T
@@ -828,6 +830,7 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
     return e;
   };
   CK(alloc_pl(c->X, R * c->ldX, true));
+  CK(alloc_pl(c->Xenv, (size_t)E * c->ldX, true));
   c->act.resize(cfg->hidden_layers);
   for (auto& p : c->act) CK(alloc_pl(p, R * wd, true));
   c->ldz = r4(H);
@@ -954,6 +957,7 @@ hrp_status hrp_env_reset(hrp_ctx* c, const uint8_t* d_windows) {
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->win, d_windows, (size_t)c->cfg.n_envs * c->hs.W, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemsetAsync(c->sched, 0, sizeof(uint64_t) * c->cfg.n_envs, c->stream));
+  c->xenv_valid = false;
   return HRP_OK;
 }
 
@@ -967,11 +971,14 @@ hrp_status hrp_env_step(hrp_ctx* c, uint64_t thr, const uint32_t* d_u_explore,
   CK(cudaSetDevice(c->device));
   const int E = c->cfg.n_envs;
   hrp_status s;
-  prof_begin(c);
-  encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool, c->X.hi,
-                                                     c->X.lo, c->ldX);
-  if ((s = launch_check(c, HRP_K_ENCODE))) return s;
-  if ((s = mlp_forward(c, c->theta, c->X, E, c->z, 0, nullptr, 0, c->ldz))) return s;
+  if (!c->xenv_valid) {   // else the last update encoded these states (on its side stream)
+    prof_begin(c);
+    encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool,
+                                                       c->Xenv.hi, c->Xenv.lo, c->ldX);
+    if ((s = launch_check(c, HRP_K_ENCODE))) return s;
+  }
+  c->xenv_valid = false;   // the step changes the states
+  if ((s = mlp_forward(c, c->theta, c->Xenv, E, c->z, 0, nullptr, 0, c->ldz))) return s;
   SelArgs a{};
   a.M = E;
   a.z = c->z;
@@ -1048,6 +1055,24 @@ hrp_status dqn_grad(hrp_ctx* c, const uint32_t* d_u_replay, float* d_loss, int64
   const int64_t nf = std::min<int64_t>(c->cfg.replay_capacity, c->inserted);
   const int H = c->hs.head_width();
   hrp_status s;
+  {
+    // the next env step's input: the environments' current states do not change during the
+    // update, so they are encoded now, off the env step's critical path (side stream)
+    const int E = c->cfg.n_envs;
+    auto enc = [&]() -> hrp_status {
+      prof_begin(c);
+      encode_kernel<<<(E + 7) / 8, 256, 0, c->stream>>>(E, c->hs.W, c->win, c->sched, c->dt.pool,
+                                                         c->Xenv.hi, c->Xenv.lo, c->ldX);
+      return launch_check(c, HRP_K_ENCODE);
+    };
+    if (concurrent(c)) {
+      if ((s = fork(c))) return s;
+      if ((s = on_side(c, enc))) return s;
+    } else if ((s = enc())) {
+      return s;
+    }
+    c->xenv_valid = true;
+  }
   prof_begin(c);
   // replay sample + encoding of s and s' in one launch, one warp per sample (the per-sample
   // decode is latency-bound: 8 samples per 256-thread CTA spreads it over the SMs)
