@@ -241,6 +241,10 @@ struct hrp_ctx {
   // pair is CUDA-graph capturable.  Not used while per-kernel profiling is on.
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // second side stream: the duelling head's weight gradient (scatter / su / finalize) beside
+  // the hidden layers' weight gradients on `side` and the data-gradient chain on the main stream
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   std::vector<Pl> act_t;              // target-pass hidden outputs [B][w] (concurrent scratch)
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
@@ -330,12 +334,16 @@ struct hrp_ctx {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
     if (side) cudaStreamSynchronize(side);
+    if (side2) cudaStreamSynchronize(side2);
     if (comm) ncclCommDestroy(comm);
     if (tc) tc_gemm_destroy(tc);
     for (auto e : ev_pool) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (side2) cudaStreamDestroy(side2);
+    if (ev_fork2) cudaEventDestroy(ev_fork2);
+    if (ev_join2) cudaEventDestroy(ev_join2);
     ar.release();
   }
 };
@@ -538,7 +546,10 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     h.acc = c->hacc; h.accU = c->haccU;
     h.gW = c->grad + c->woff[nl - 1];
     h.gb = h.gW + (int64_t)w * H;
-    if (conc && (s = fork(c))) return s;
+    if (conc) {   // main -> side2
+      CK(cudaEventRecord(c->ev_fork2, c->stream));
+      CK(cudaStreamWaitEvent(c->side2, c->ev_fork2, 0));
+    }
     auto wgrad = [&]() -> hrp_status {
       CK(cudaMemsetAsync(c->hacc, 0, sizeof(double) * (size_t)H * (w + 1), c->stream));
       const int spc = std::max(4, std::min(64, B / (4 * 148) + 1));
@@ -553,9 +564,18 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
       prof_begin(c);
       head_finalize_kernel<<<(int)std::min<int64_t>(4 * 148, (n + 255) / 256), 256, 0, c->stream>>>(h);
       if ((t = launch_check(c, HRP_K_HEAD_BWD))) return t;
-      return allreduce_layer(c, nl - 1);
+      // the head's gradient bucket is allreduced after the hidden layers' (on `side`, below),
+      // so every NCCL call of the update stays on one stream, in the same order on every rank
+      return conc ? HRP_OK : allreduce_layer(c, nl - 1);
     };
-    s = conc ? on_side(c, wgrad) : wgrad();
+    if (conc) {
+      cudaStream_t m = c->stream;
+      c->stream = c->side2;
+      s = wgrad();
+      c->stream = m;
+    } else {
+      s = wgrad();
+    }
     if (s) return s;
     prof_begin(c);
     head_dgrad_kernel<<<dim3((w + kHeadCols - 1) / kHeadCols, (B + kHeadRows - 1) / kHeadRows), 256,
@@ -597,7 +617,13 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
       ldy = fi;
     }
   }
-  if (conc && (s = join(c))) return s;
+  if (conc) {
+    // the head's bucket: side waits for side2's head gradient, allreduces it; then main joins both
+    CK(cudaEventRecord(c->ev_join2, c->side2));
+    CK(cudaStreamWaitEvent(c->side, c->ev_join2, 0));
+    if ((s = on_side(c, [&]() { return allreduce_layer(c, nl - 1); }))) return s;
+    if ((s = join(c))) return s;
+  }
   return HRP_OK;
 }
 
@@ -880,6 +906,9 @@ hrp_status hrp_env_create(const hrp_space* space, const hrp_profiles* prof,
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming));
   CK(ar.alloc((void**)&c->bwin, R * W));
   CK(ar.alloc((void**)&c->bsched, R * 8));
   CK(ar.alloc((void**)&c->bact, R * 8));
