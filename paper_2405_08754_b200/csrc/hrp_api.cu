@@ -524,6 +524,9 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
   const int H = c->dims[nl];
   const int Bp = c->Bp;
   const bool conc = concurrent(c);
+  // the second side stream pays off from batches of ~1k samples (at cfg 1's 64 its fork / join
+  // cost more than the overlap gains)
+  const bool conc2 = conc && B >= 1024;
   hrp_status s;
   Pl dY, dYT;
   int ldy = 0;
@@ -546,9 +549,11 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
     h.acc = c->hacc; h.accU = c->haccU;
     h.gW = c->grad + c->woff[nl - 1];
     h.gb = h.gW + (int64_t)w * H;
-    if (conc) {   // main -> side2
+    if (conc2) {   // main -> side2
       CK(cudaEventRecord(c->ev_fork2, c->stream));
       CK(cudaStreamWaitEvent(c->side2, c->ev_fork2, 0));
+    } else if (conc && (s = fork(c))) {   // main -> side
+      return s;
     }
     auto wgrad = [&]() -> hrp_status {
       CK(cudaMemsetAsync(c->hacc, 0, sizeof(double) * (size_t)H * (w + 1), c->stream));
@@ -566,15 +571,15 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
       if ((t = launch_check(c, HRP_K_HEAD_BWD))) return t;
       // the head's gradient bucket is allreduced after the hidden layers' (on `side`, below),
       // so every NCCL call of the update stays on one stream, in the same order on every rank
-      return conc ? HRP_OK : allreduce_layer(c, nl - 1);
+      return conc2 ? HRP_OK : allreduce_layer(c, nl - 1);
     };
-    if (conc) {
+    if (conc2) {
       cudaStream_t m = c->stream;
       c->stream = c->side2;
       s = wgrad();
       c->stream = m;
     } else {
-      s = wgrad();
+      s = conc ? on_side(c, wgrad) : wgrad();
     }
     if (s) return s;
     prof_begin(c);
@@ -617,13 +622,13 @@ hrp_status mlp_backward(hrp_ctx* c, int B) {
       ldy = fi;
     }
   }
-  if (conc) {
-    // the head's bucket: side waits for side2's head gradient, allreduces it; then main joins both
+  if (conc2) {
+    // the head's bucket: side waits for side2's head gradient, allreduces it
     CK(cudaEventRecord(c->ev_join2, c->side2));
     CK(cudaStreamWaitEvent(c->side, c->ev_join2, 0));
     if ((s = on_side(c, [&]() { return allreduce_layer(c, nl - 1); }))) return s;
-    if ((s = join(c))) return s;
   }
+  if (conc && (s = join(c))) return s;
   return HRP_OK;
 }
 
